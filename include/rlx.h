@@ -1,0 +1,198 @@
+/*
+ * rlx.h — C-ABI of the B200 look-ahead candidate evaluator.
+ *
+ * The reference (`rlmux`, pure Python) has no FFI; its de-facto seam for
+ * this hot path is the chooser callable handed to `_drive`
+ * (rlmux/scheduler.py:925-950, chooser at :963-972) together with the
+ * module-global `enumerate_actions` (:648-703) it scores through
+ * `candidate_cost` (:902-918) and `action_finish_estimate` (:773-789).
+ * These entry points replace exactly that seam:
+ *
+ *   rlx_open / rlx_close           handle + device buffers (one handle per GPU / rank)
+ *   rlx_load_instance              static per-instance data: pipelines, knobs, slowdown
+ *                                  LUT (replaces SlowdownModel.slowdown, slowdown.py:129-156)
+ *   rlx_decide                     one chooser call: enumerate + score + argmin over a
+ *                                  serial range (replaces scheduler.py:939-940 and :963-972)
+ *   rlx_decode                     serial -> action (so every rank can materialise the
+ *                                  global winner after the cross-GPU min-loc)
+ *   rlx_last_error                 text of the last failure
+ *
+ * All arrays are plain host pointers owned by the caller and only read
+ * during the call. Times are IEEE-754 binary64 seconds; every cost/finish
+ * value is bit-identical to the reference's Python float arithmetic.
+ */
+#ifndef RLX_H
+#define RLX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLX_ABI_VERSION 1
+
+/* Kind codes = declaration order of rlmux SubStageKind (graph.py:69-76). */
+enum {
+  RLX_KIND_PREFILL_BURST = 0,
+  RLX_KIND_DECODE_LARGE = 1,
+  RLX_KIND_DECODE_MEDIUM = 2,
+  RLX_KIND_DECODE_SMALL = 3,
+  RLX_KIND_REFERENCE = 4,
+  RLX_KIND_TRAINING = 5,
+  RLX_KIND_TOOL_WAIT = 6,
+  RLX_NKIND = 7
+};
+
+/* Allocation index space of the slowdown LUT.
+ *   0            FULL_ALLOCATION (1.0, 0.8)                       slowdown.py:52
+ *   1 + 4*i + j  Multiplex alloc (MUX_SM_GRID[i], MEM_GRID[j])    scheduler.py:46, :671-675
+ *   13 + 4*i + j complement_allocation of the above                slowdown.py:169-175
+ * LUT layout: lut[(kind * 8 + partner) * RLX_NALLOC + alloc], partner 0 = None,
+ * partner k+1 = kind k. A NaN entry marks a (kind, partner) pair missing from
+ * the table (the reference raises KeyError on use, slowdown.py:143-147). */
+#define RLX_NALLOC 25
+#define RLX_NPARTNER 8
+
+/* Candidate classes = reference priorities (scheduler.py:644). */
+enum { RLX_CLASS_MULTIPLEX = 0, RLX_CLASS_MERGE = 1, RLX_CLASS_EXCLUSIVE = 2 };
+
+/* Status codes. */
+enum {
+  RLX_OK = 0,
+  RLX_ERR_ARG = 1,         /* bad argument / malformed state                       */
+  RLX_ERR_CUDA = 2,        /* CUDA runtime / device failure                        */
+  RLX_ERR_SCHEDULING = 3,  /* reference SchedulingError (e.g. window guard, :866) */
+  RLX_ERR_KEY = 4,         /* reference KeyError (missing slowdown row / latency)  */
+  RLX_ERR_LIMIT = 5,       /* outside this build's compiled limits                 */
+  RLX_ERR_VALUE = 6        /* reference ValueError                                 */
+};
+
+#define RLX_MAX_MEMBERS 64
+
+typedef struct RlxInstanceDesc {
+  int32_t abi_version;           /* = RLX_ABI_VERSION */
+  int32_t n_pipes;
+  const char* pipe_names;        /* NUL-separated pipeline ids, pipe p at pipe_name_off[p] */
+  const int32_t* pipe_name_off;
+  const double* latency;         /* [n_pipes*3] latency_model[bucket] for buckets 0..2     */
+  const uint8_t* latency_ok;     /* [n_pipes*3] 1 if that bucket key exists              */
+  const uint8_t* has_spec;       /* [n_pipes] PipelineSpec present                        */
+  const double* model_params;    /* [n_pipes]                                             */
+  const double* peak_flops;      /* [n_pipes]                                             */
+  const double* prefill_mfu;     /* [n_pipes]                                             */
+  int32_t n_workers;
+  const int32_t* worker_ids;     /* [n_workers] ascending (Instance.workers(), :135-139)  */
+  double headroom;
+  double realloc_penalty;
+  double default_migration_cost;
+  int32_t merge_enabled;
+  int32_t _pad;
+  const double* lut;             /* [RLX_NKIND * RLX_NPARTNER * RLX_NALLOC]               */
+  const double* alloc_sm;        /* [RLX_NALLOC] sm share of each allocation index        */
+  const double* alloc_mem;       /* [RLX_NALLOC] mem share of each allocation index       */
+} RlxInstanceDesc;
+
+/* Snapshot of ExecState (scheduler.py:339-366) at a decision point.
+ * Nodes are the alive sub-stages (completed ones included); node index =
+ * position in these arrays. */
+typedef struct RlxStateDesc {
+  double now;
+  int32_t n_nodes;
+  int32_t n_edges;
+  const int32_t* pipe;           /* [n] pipeline index                                    */
+  const int32_t* worker;         /* [n] dense worker index into worker_ids                */
+  const int32_t* kind;           /* [n] RLX_KIND_*                                        */
+  const double* duration;        /* [n]                                                   */
+  const double* mem;             /* [n] mem_fraction                                      */
+  const int64_t* remaining;      /* [n] remaining_decode_tokens                           */
+  const int64_t* active;         /* [n] active_requests                                   */
+  const int64_t* context;        /* [n] context_tokens                                    */
+  const uint8_t* completed;      /* [n]                                                   */
+  const double* merge_prefix;    /* [n] pending merge prefix (0 if none)                  */
+  const char* ids;               /* NUL-separated node ids                                */
+  const int32_t* id_off;         /* [n]                                                   */
+  const int32_t* edge_src;       /* [n_edges]                                             */
+  const int32_t* edge_dst;       /* [n_edges]                                             */
+  int32_t n_running;
+  int32_t n_toolwaits;
+  const int32_t* run_node;       /* [n_running]                                           */
+  const int32_t* run_partner;    /* [n_running] node index of the partner, -1 if none     */
+  const double* run_rate;
+  const double* run_prefix;
+  const double* run_work;
+  const int32_t* tw_node;        /* [n_toolwaits] running tool waits                      */
+  const double* tw_end;
+  int32_t n_grants;              /* last_mem_grant entries (realloc penalty)              */
+  int32_t _pad;
+  const int32_t* grant_worker;   /* dense worker index                                    */
+  const int32_t* grant_pipe;
+  const double* grant_mem;
+} RlxStateDesc;
+
+typedef struct RlxDecideArgs {
+  int32_t window;                /* look-ahead depth W >= 1                               */
+  int32_t max_merge;             /* merge-set size cap; <= 0 means uncapped (reference)   */
+  int64_t serial_begin;          /* shard [begin, end) of the global serial range;        */
+  int64_t serial_end;            /*   end < 0 means "to the last candidate"               */
+  double* keys_out;              /* optional host [2*(end-begin)]: (cost, finish) per     */
+                                 /*   candidate, for parity tests                         */
+  void* dev_key_out;             /* optional DEVICE pointer to 4 x uint64 that receives   */
+                                 /*   the shard's packed best key (for the NCCL min-loc)  */
+  int32_t flags;                 /* RLX_F_*                                               */
+  int32_t _pad;
+} RlxDecideArgs;
+
+#define RLX_F_NO_SYNC_STATS 1     /* skip the stats readback */
+
+/* Packed key: cost and finish are non-negative doubles, so their bit
+ * patterns order as uint64; word 2 = priority << 61 | serial; word 3 = 1 if
+ * valid. Lexicographic order over words 0..2 == the reference's
+ * (cost, finish, priority, serial) tuple order (scheduler.py:969). */
+typedef struct RlxKey {
+  uint64_t cost_bits;
+  uint64_t finish_bits;
+  uint64_t prio_serial;
+  uint64_t valid;
+} RlxKey;
+
+typedef struct RlxAction {
+  int32_t cls;                   /* RLX_CLASS_*                                           */
+  int32_t node_a;                /* Exclusive node / Multiplex first                      */
+  int32_t node_b;                /* Multiplex second                                      */
+  int32_t alloc;                 /* alloc index of node_a (0 for Exclusive)               */
+  int32_t target_worker;         /* Merge target (dense worker index)                     */
+  int32_t n_members;             /* Merge members, node indices in sorted-id order        */
+  int32_t members[RLX_MAX_MEMBERS];
+} RlxAction;
+
+typedef struct RlxDecision {
+  int64_t n_candidates;          /* total candidates at this decision (all shards)        */
+  int32_t found;                 /* shard had >= 1 candidate                              */
+  int32_t priority;
+  int64_t serial;
+  double cost;
+  double finish;
+  RlxAction action;              /* decoded winner of this shard                          */
+  RlxKey key;
+  /* measurement */
+  int64_t passes;                /* list-scheduling passes run                            */
+  double alg_bytes;              /* SURVEY §8(d) algorithmic bytes of the scored shard    */
+  double kernel_ms;              /* device time of the scoring kernel (CUDA events)       */
+  double plan_ms;                /* host planning time                                    */
+  int64_t n_merge, n_multiplex, n_exclusive;
+} RlxDecision;
+
+int rlx_abi_version(void);
+int rlx_open(int device, void** handle);
+int rlx_load_instance(void* handle, const RlxInstanceDesc* inst);
+int rlx_decide(void* handle, const RlxStateDesc* state, const RlxDecideArgs* args, RlxDecision* out);
+int rlx_decode(void* handle, int64_t serial, RlxAction* out);
+const char* rlx_last_error(void* handle);
+void rlx_close(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RLX_H */

@@ -1,0 +1,99 @@
+"""ctypes mirror of include/rlx.h (the C-ABI boundary)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+RLX_ABI_VERSION = 1
+RLX_NKIND = 7
+RLX_NALLOC = 25
+RLX_NPARTNER = 8
+RLX_MAX_MEMBERS = 64
+
+RLX_OK, RLX_ERR_ARG, RLX_ERR_CUDA, RLX_ERR_SCHEDULING, RLX_ERR_KEY, RLX_ERR_LIMIT, RLX_ERR_VALUE = range(7)
+CLASS_MULTIPLEX, CLASS_MERGE, CLASS_EXCLUSIVE = 0, 1, 2
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+_bp = C.POINTER(C.c_uint8)
+
+
+class RlxInstanceDesc(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_int32), ("n_pipes", C.c_int32),
+        ("pipe_names", C.c_char_p), ("pipe_name_off", _ip),
+        ("latency", _dp), ("latency_ok", _bp), ("has_spec", _bp),
+        ("model_params", _dp), ("peak_flops", _dp), ("prefill_mfu", _dp),
+        ("n_workers", C.c_int32), ("worker_ids", _ip),
+        ("headroom", C.c_double), ("realloc_penalty", C.c_double), ("default_migration_cost", C.c_double),
+        ("merge_enabled", C.c_int32), ("_pad", C.c_int32),
+        ("lut", _dp), ("alloc_sm", _dp), ("alloc_mem", _dp),
+    ]
+
+
+class RlxStateDesc(C.Structure):
+    _fields_ = [
+        ("now", C.c_double), ("n_nodes", C.c_int32), ("n_edges", C.c_int32),
+        ("pipe", _ip), ("worker", _ip), ("kind", _ip), ("duration", _dp), ("mem", _dp),
+        ("remaining", _lp), ("active", _lp), ("context", _lp), ("completed", _bp), ("merge_prefix", _dp),
+        ("ids", C.c_char_p), ("id_off", _ip), ("edge_src", _ip), ("edge_dst", _ip),
+        ("n_running", C.c_int32), ("n_toolwaits", C.c_int32),
+        ("run_node", _ip), ("run_partner", _ip), ("run_rate", _dp), ("run_prefix", _dp), ("run_work", _dp),
+        ("tw_node", _ip), ("tw_end", _dp),
+        ("n_grants", C.c_int32), ("_pad", C.c_int32),
+        ("grant_worker", _ip), ("grant_pipe", _ip), ("grant_mem", _dp),
+    ]
+
+
+class RlxDecideArgs(C.Structure):
+    _fields_ = [
+        ("window", C.c_int32), ("max_merge", C.c_int32),
+        ("serial_begin", C.c_int64), ("serial_end", C.c_int64),
+        ("keys_out", _dp), ("dev_key_out", C.c_void_p),
+        ("flags", C.c_int32), ("_pad", C.c_int32),
+    ]
+
+
+class RlxKey(C.Structure):
+    _fields_ = [("cost_bits", C.c_uint64), ("finish_bits", C.c_uint64), ("prio_serial", C.c_uint64),
+                ("valid", C.c_uint64)]
+
+
+class RlxAction(C.Structure):
+    _fields_ = [("cls", C.c_int32), ("node_a", C.c_int32), ("node_b", C.c_int32), ("alloc", C.c_int32),
+                ("target_worker", C.c_int32), ("n_members", C.c_int32),
+                ("members", C.c_int32 * RLX_MAX_MEMBERS)]
+
+
+class RlxDecision(C.Structure):
+    _fields_ = [
+        ("n_candidates", C.c_int64), ("found", C.c_int32), ("priority", C.c_int32), ("serial", C.c_int64),
+        ("cost", C.c_double), ("finish", C.c_double), ("action", RlxAction), ("key", RlxKey),
+        ("passes", C.c_int64), ("alg_bytes", C.c_double), ("kernel_ms", C.c_double), ("plan_ms", C.c_double),
+        ("n_merge", C.c_int64), ("n_multiplex", C.c_int64), ("n_exclusive", C.c_int64),
+    ]
+
+
+# Every symbol include/rlx.h declares (checked by tests/test_abi.py).
+EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "rlx_decode",
+            "rlx_last_error", "rlx_close")
+
+
+def bind(lib: C.CDLL) -> C.CDLL:
+    lib.rlx_abi_version.restype = C.c_int
+    lib.rlx_abi_version.argtypes = []
+    lib.rlx_open.restype = C.c_int
+    lib.rlx_open.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    lib.rlx_load_instance.restype = C.c_int
+    lib.rlx_load_instance.argtypes = [C.c_void_p, C.POINTER(RlxInstanceDesc)]
+    lib.rlx_decide.restype = C.c_int
+    lib.rlx_decide.argtypes = [C.c_void_p, C.POINTER(RlxStateDesc), C.POINTER(RlxDecideArgs),
+                               C.POINTER(RlxDecision)]
+    lib.rlx_decode.restype = C.c_int
+    lib.rlx_decode.argtypes = [C.c_void_p, C.c_int64, C.POINTER(RlxAction)]
+    lib.rlx_last_error.restype = C.c_char_p
+    lib.rlx_last_error.argtypes = [C.c_void_p]
+    lib.rlx_close.restype = None
+    lib.rlx_close.argtypes = [C.c_void_p]
+    return lib
