@@ -1,0 +1,340 @@
+// rlx_abi.cu — the C-ABI of include/rlx.h.
+//
+// One handle per GPU. rlx_decide = host plan (rlx_plan.cpp) -> one H2D copy
+// of the plan blob -> persistent scoring kernel over the requested serial
+// shard -> deterministic reduce -> 7-word result D2H. The packed shard key
+// can also be left in device memory (dev_key_out) for the cross-GPU
+// lexicographic min-loc collective.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../../include/rlx.h"
+#include "rlx_hostplan.hpp"
+
+
+using namespace rlx;
+
+namespace {
+
+constexpr int kMaxSlices = 1 << 16;
+constexpr size_t kSliceOutBytes = 48;
+
+struct Handle {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::string err;
+  // owned instance copy
+  bool loaded = false;
+  RlxInstanceDesc inst{};
+  std::string pipe_names;
+  std::vector<int32_t> pipe_name_off, worker_ids;
+  std::vector<double> latency, params, peak, mfu, lut, alloc_sm, alloc_mem;
+  std::vector<uint8_t> latency_ok, has_spec;
+  // plan
+  HostPlan hp;
+  bool have_plan = false;
+  DevPlan host_view{};
+  // device buffers
+  uint8_t* d_blob = nullptr;
+  size_t blob_cap = 0;
+  uint8_t* h_pin = nullptr;
+  size_t pin_cap = 0;
+  uint8_t* d_outs = nullptr;
+  unsigned long long* d_counter = nullptr;
+  int* d_err = nullptr;
+  unsigned long long* d_res = nullptr;
+  unsigned long long* h_res = nullptr;
+  double* d_keys = nullptr;
+  size_t keys_cap = 0;
+  double* d_dbg = nullptr;
+  double h_dbg[16];
+  int threads_hint = 0;
+};
+
+int fail(Handle* h, int code, const std::string& msg) {
+  h->err = msg;
+  return code;
+}
+
+int cuda_fail(Handle* h, cudaError_t e, const char* where) {
+  h->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return RLX_ERR_CUDA;
+}
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t _e = (x);                       \
+    if (_e != cudaSuccess) return cuda_fail(h, _e, #x); \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int rlx_abi_version(void) { return RLX_ABI_VERSION; }
+
+int rlx_open(int device, void** handle) {
+  if (!handle) return RLX_ERR_ARG;
+  *handle = nullptr;
+  Handle* h = new Handle();
+  h->device = device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev <= device || device < 0) {
+    delete h;
+    return RLX_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete h;
+    return RLX_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&h->e0) != cudaSuccess || cudaEventCreate(&h->e1) != cudaSuccess ||
+      cudaMalloc(&h->d_outs, kSliceOutBytes * kMaxSlices) != cudaSuccess ||
+      cudaMalloc(&h->d_counter, 64) != cudaSuccess || cudaMalloc(&h->d_err, 64) != cudaSuccess ||
+      cudaMalloc(&h->d_res, 64) != cudaSuccess || cudaMallocHost(&h->h_res, 64) != cudaSuccess ||
+      cudaMalloc(&h->d_dbg, 16 * sizeof(double)) != cudaSuccess) {
+    delete h;
+    return RLX_ERR_CUDA;
+  }
+  const char* th = getenv("RLX_THREADS");
+  if (th) h->threads_hint = atoi(th);
+  *handle = h;
+  return RLX_OK;
+}
+
+int rlx_load_instance(void* handle, const RlxInstanceDesc* in) {
+  Handle* h = (Handle*)handle;
+  if (!h || !in) return RLX_ERR_ARG;
+  if (in->abi_version != RLX_ABI_VERSION) return fail(h, RLX_ERR_ARG, "ABI version mismatch");
+  const int P = in->n_pipes, W = in->n_workers;
+  if (P <= 0 || W <= 0) return fail(h, RLX_ERR_ARG, "empty instance");
+  size_t names_len = 0;
+  for (int p = 0; p < P; p++) {
+    size_t e = in->pipe_name_off[p] + strlen(in->pipe_names + in->pipe_name_off[p]) + 1;
+    if (e > names_len) names_len = e;
+  }
+  h->pipe_names.assign(in->pipe_names, names_len);
+  h->pipe_name_off.assign(in->pipe_name_off, in->pipe_name_off + P);
+  h->latency.assign(in->latency, in->latency + 3 * P);
+  h->latency_ok.assign(in->latency_ok, in->latency_ok + 3 * P);
+  h->has_spec.assign(in->has_spec, in->has_spec + P);
+  h->params.assign(in->model_params, in->model_params + P);
+  h->peak.assign(in->peak_flops, in->peak_flops + P);
+  h->mfu.assign(in->prefill_mfu, in->prefill_mfu + P);
+  h->worker_ids.assign(in->worker_ids, in->worker_ids + W);
+  h->lut.assign(in->lut, in->lut + RLX_NKIND * RLX_NPARTNER * RLX_NALLOC);
+  h->alloc_sm.assign(in->alloc_sm, in->alloc_sm + RLX_NALLOC);
+  h->alloc_mem.assign(in->alloc_mem, in->alloc_mem + RLX_NALLOC);
+  for (int p = 0; p < P; p++)
+    if (h->has_spec[p] && !(h->mfu[p] > 0)) return fail(h, RLX_ERR_VALUE, "prefill_mfu must be positive");
+  RlxInstanceDesc& d = h->inst;
+  d = *in;
+  d.pipe_names = h->pipe_names.data();
+  d.pipe_name_off = h->pipe_name_off.data();
+  d.latency = h->latency.data();
+  d.latency_ok = h->latency_ok.data();
+  d.has_spec = h->has_spec.data();
+  d.model_params = h->params.data();
+  d.peak_flops = h->peak.data();
+  d.prefill_mfu = h->mfu.data();
+  d.worker_ids = h->worker_ids.data();
+  d.lut = h->lut.data();
+  d.alloc_sm = h->alloc_sm.data();
+  d.alloc_mem = h->alloc_mem.data();
+  h->loaded = true;
+  h->have_plan = false;
+  return RLX_OK;
+}
+
+static void fill_action(Handle* h, const Cand& c, RlxAction* out) {
+  memset(out, 0, sizeof *out);
+  out->cls = c.cls;
+  const std::vector<int>& l2g = h->hp.l2g;
+  if (c.cls == RLX_CLASS_MERGE) {
+    out->n_members = c.k;
+    for (int i = 0; i < c.k; i++) out->members[i] = l2g[c.m[i]];
+    out->target_worker = c.target;
+    out->node_a = out->node_b = -1;
+  } else {
+    out->node_a = l2g[c.a];
+    out->node_b = c.cls == RLX_CLASS_MULTIPLEX ? l2g[c.b] : -1;
+    out->alloc = c.alloc;
+  }
+}
+
+int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, RlxDecision* out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !sd || !args || !out) return RLX_ERR_ARG;
+  if (!h->loaded) return fail(h, RLX_ERR_ARG, "no instance loaded");
+  if (args->window < 1) return fail(h, RLX_ERR_VALUE, "window must be >= 1");
+  memset(out, 0, sizeof *out);
+  out->serial = -1;
+  CK(cudaSetDevice(h->device));
+  auto t0 = std::chrono::steady_clock::now();
+  h->have_plan = false;
+  int rc = build_plan(&h->inst, sd, args->window, args->max_merge, h->hp, h->err);
+  if (rc) return rc;
+  h->have_plan = true;
+  relocate(h->hp, h->hp.blob.buf.data(), h->host_view);
+  const DevPlan& hv = h->host_view;
+  out->n_candidates = hv.n_total;
+  out->n_merge = hv.n_merge;
+  out->n_multiplex = hv.n_mux;
+  out->n_exclusive = hv.n_excl;
+  int64_t b = args->serial_begin < 0 ? 0 : args->serial_begin;
+  int64_t e = args->serial_end < 0 ? hv.n_total : args->serial_end;
+  if (e > hv.n_total) e = hv.n_total;
+  if (b > e) b = e;
+  auto t1 = std::chrono::steady_clock::now();
+  out->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  if (e == b) {
+    if (args->dev_key_out) {
+      CK(cudaMemsetAsync(args->dev_key_out, 0xFF, 24, h->stream));
+      CK(cudaMemsetAsync((uint8_t*)args->dev_key_out + 24, 0, 8, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    return RLX_OK;
+  }
+  // ---- upload plan
+  size_t nb = h->hp.blob.buf.size();
+  if (nb > h->pin_cap) {
+    if (h->h_pin) cudaFreeHost(h->h_pin);
+    h->pin_cap = nb * 2;
+    CK(cudaMallocHost(&h->h_pin, h->pin_cap));
+  }
+  if (nb > h->blob_cap) {
+    if (h->d_blob) cudaFree(h->d_blob);
+    h->blob_cap = nb * 2;
+    CK(cudaMalloc(&h->d_blob, h->blob_cap));
+  }
+  memcpy(h->h_pin, h->hp.blob.buf.data(), nb);
+  CK(cudaMemcpyAsync(h->d_blob, h->h_pin, nb, cudaMemcpyHostToDevice, h->stream));
+  DevPlan dp;
+  relocate(h->hp, h->d_blob, dp);
+  // ---- work ranges: merges first (heaviest), then multiplex, then exclusive
+  WorkDesc wd;
+  memset(&wd, 0, sizeof wd);
+  auto clip = [&](int64_t lo, int64_t hi, int64_t& s, int64_t& n) {
+    int64_t x = lo > b ? lo : b, y = hi < e ? hi : e;
+    s = x;
+    n = y > x ? y - x : 0;
+  };
+  clip(hv.n_mux, hv.n_mux + hv.n_merge, wd.a0, wd.na);
+  clip(0, hv.n_mux, wd.b0, wd.nb);
+  clip(hv.n_mux + hv.n_merge, hv.n_total, wd.c0, wd.nc);
+  wd.shard0 = b;
+  wd.counter = h->d_counter;
+  wd.err = h->d_err;
+  if (args->keys_out) {
+    size_t need = sizeof(double) * 2 * (size_t)(e - b);
+    if (need > h->keys_cap) {
+      if (h->d_keys) cudaFree(h->d_keys);
+      h->keys_cap = need;
+      CK(cudaMalloc(&h->d_keys, need));
+    }
+    wd.keys_out = h->d_keys;
+  }
+  CK(cudaMemsetAsync(h->d_counter, 0, 8, h->stream));
+  CK(cudaMemsetAsync(h->d_err, 0, 4, h->stream));
+  CK(cudaMemsetAsync(h->d_dbg, 0, 16 * sizeof(double), h->stream));
+  wd.dbg = h->d_dbg;
+  int n_slices = 0;
+  CK(cudaEventRecord(h->e0, h->stream));
+  rc = launch_score(dp, wd, (SliceOut*)h->d_outs, kMaxSlices, h->sm_count, h->stream, &n_slices, h->threads_hint);
+  if (rc) return fail(h, rc, rc == RLX_ERR_LIMIT ? "plan does not fit in shared memory" : "kernel launch failed");
+  CK(cudaEventRecord(h->e1, h->stream));
+  rc = launch_reduce((SliceOut*)h->d_outs, n_slices, h->d_res, h->stream);
+  if (rc) return fail(h, rc, "reduce launch failed");
+  if (args->dev_key_out)
+    CK(cudaMemcpyAsync(args->dev_key_out, h->d_res, 32, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->h_res, h->d_res, 56, cudaMemcpyDeviceToHost, h->stream));
+  int herr = 0;
+  CK(cudaMemcpyAsync(&h->h_res[7], h->d_err, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  herr = (int)(h->h_res[7] & 0xffffffffu);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->e0, h->e1);
+  out->kernel_ms = ms;
+  if (herr) {
+    if (herr == RLX_ERR_SCHEDULING) {
+      cudaMemcpy(h->h_dbg, h->d_dbg, sizeof h->h_dbg, cudaMemcpyDeviceToHost);
+      char buf[400];
+      snprintf(buf, sizeof buf,
+               "window estimate did not converge (serial %.0f variant %.0f now %.17g done %.0f/%.0f tw_run %.0f "
+               "tw_live %.0f twq %.0f nm0 %.0f act %.0f/%.0f mt %.0f)",
+               h->h_dbg[1], h->h_dbg[2], h->h_dbg[3], h->h_dbg[4], h->h_dbg[5], h->h_dbg[6], h->h_dbg[7],
+               h->h_dbg[8], h->h_dbg[9], h->h_dbg[10], h->h_dbg[11], h->h_dbg[12]);
+      return fail(h, herr, buf);
+    }
+    if (herr == RLX_ERR_KEY) return fail(h, herr, "slowdown table or latency model has no entry for a queried pair");
+    return fail(h, herr, "device error");
+  }
+  unsigned long long* r = h->h_res;
+  out->key.cost_bits = r[0];
+  out->key.finish_bits = r[1];
+  out->key.prio_serial = r[2];
+  out->key.valid = r[3];
+  out->passes = (int64_t)r[4];
+  double by;
+  memcpy(&by, &r[5], 8);
+  out->alg_bytes = by;
+  if (r[3]) {
+    out->found = 1;
+    memcpy(&out->cost, &r[0], 8);
+    memcpy(&out->finish, &r[1], 8);
+    out->priority = (int)(r[2] >> 61);
+    out->serial = (int64_t)(r[2] & ((1ull << 61) - 1));
+    Cand c;
+    decode_serial(hv, out->serial, c);
+    fill_action(h, c, &out->action);
+  }
+  if (args->keys_out)
+    CK(cudaMemcpy(args->keys_out, h->d_keys, sizeof(double) * 2 * (size_t)(e - b), cudaMemcpyDeviceToHost));
+  return RLX_OK;
+}
+
+int rlx_decode(void* handle, int64_t serial, RlxAction* out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !out) return RLX_ERR_ARG;
+  if (!h->have_plan) return fail(h, RLX_ERR_ARG, "rlx_decode needs a preceding rlx_decide on the same state");
+  Cand c;
+  if (!decode_serial(h->host_view, serial, c)) return fail(h, RLX_ERR_ARG, "serial out of range");
+  fill_action(h, c, out);
+  return RLX_OK;
+}
+
+const char* rlx_last_error(void* handle) {
+  Handle* h = (Handle*)handle;
+  return h ? h->err.c_str() : "null handle";
+}
+
+void rlx_close(void* handle) {
+  Handle* h = (Handle*)handle;
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->d_blob) cudaFree(h->d_blob);
+  if (h->h_pin) cudaFreeHost(h->h_pin);
+  if (h->d_outs) cudaFree(h->d_outs);
+  if (h->d_counter) cudaFree(h->d_counter);
+  if (h->d_err) cudaFree(h->d_err);
+  if (h->d_res) cudaFree(h->d_res);
+  if (h->h_res) cudaFreeHost(h->h_res);
+  if (h->d_keys) cudaFree(h->d_keys);
+  if (h->d_dbg) cudaFree(h->d_dbg);
+  if (h->e0) cudaEventDestroy(h->e0);
+  if (h->e1) cudaEventDestroy(h->e1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

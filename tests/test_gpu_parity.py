@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA chooser (through the C-ABI) against the reference's
+golden vectors and the CPU oracle. Bit-exact: every cost / finish double
+and every selected serial must be identical."""
+
+import numpy as np
+import pytest
+
+from helpers import instance, load_gz
+from paper_2604_23838_b200 import drive, simulate
+from paper_2604_23838_b200.engine import HostState
+from paper_2604_23838_b200.instance_io import action_to_json
+from paper_2604_23838_b200.model import SchedulingError
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def Evaluator():
+    from paper_2604_23838_b200.native import Evaluator as E
+
+    return E
+
+
+def test_golden_schedules(Evaluator, golden_schedules):
+    bad = []
+    ev = None
+    for name, g in sorted(golden_schedules.items()):
+        inst = instance(g["instance"])
+        if ev is None:
+            ev = Evaluator(inst)
+        else:
+            ev.bind(inst)
+        log = []
+        s = drive(inst, ev.chooser(g["window"], g["max_merge"], log), "lookahead", {})
+        acts = [[t.start, action_to_json(t.action)] for t in s.actions]
+        ok = acts == g["actions"] and len(log) == len(g["decisions"])
+        if ok:
+            for d, gd in zip(log, g["decisions"]):
+                ok = ok and d["n"] == gd["n"] and list(d["key"]) == list(gd["key"])
+        if ok:
+            rep = simulate(s, inst)
+            ok = rep.makespan == g["makespan"] and rep.aggregate_throughput == g["throughput"]
+        if not ok:
+            first = next((i for i, (a, b) in enumerate(zip(acts, g["actions"])) if a != b), None)
+            kd = next(((i, d["key"], gd["key"]) for i, (d, gd) in enumerate(zip(log, g["decisions"]))
+                       if list(d["key"]) != list(gd["key"]) or d["n"] != gd["n"]), None)
+            bad.append((name, first, kd))
+    assert not bad, f"{len(bad)} mismatching schedules, e.g. {bad[:4]}"
+
+
+@pytest.mark.parametrize("name", ["trap", "async_small", "config1", "config2", "config3", "config4", "config5"])
+def test_golden_candidate_keys(Evaluator, golden_keys, name):
+    g = golden_keys.get(name)
+    if g is None:
+        pytest.skip("no golden keys")
+    inst = instance(g["instance"])
+    ev = Evaluator(inst)
+    st = HostState(inst)
+    if name == "config4":
+        # The reference livelocks on one merge follow-up of this decision
+        # (work_left in (EPS/rate, EPS]: consume stops, finished never
+        # holds; scheduler.py:335 vs :609) and raises SchedulingError at
+        # the 10,000-advance guard (:866). The device reproduces that, so
+        # the sampled keys are scored one serial at a time.
+        with pytest.raises(SchedulingError):
+            ev.decide(st, g["window"], g["max_merge"])
+        for serial, prio, cost, fin in g["keys"]:
+            ev.decide(st, g["window"], g["max_merge"], shard=(serial, serial + 1), want_keys=True)
+            assert (ev.keys[0, 0], ev.keys[0, 1]) == (cost, fin), (name, serial)
+        return
+    ev.decide(st, g["window"], g["max_merge"], want_keys=True)
+    assert ev.last.n_candidates == g["n_candidates"]
+    keys = ev.keys
+    for serial, prio, cost, fin in g["keys"]:
+        assert (keys[serial, 0], keys[serial, 1]) == (cost, fin), (name, serial)
+
+
+def _oracle_sample_check(inst, st, window, cap, n_sample, ev, seed=0):
+    from oracle.oracle import Oracle
+
+    d = ev.decide(st, window, cap, want_keys=True)
+    keys = ev.keys.copy()
+    n = d.n_candidates
+    rng = np.random.default_rng(seed)
+    sample = sorted(set(rng.choice(n, size=min(n_sample, n), replace=False).tolist()) | {d.serial})
+    o = Oracle(inst)
+    r = o.score(st, window, cap, serials=sample, want_keys=True)
+    assert r["n"] == n
+    for s, (oc, of) in zip(sample, r["keys"]):
+        assert (keys[s, 0], keys[s, 1]) == (oc, of), s
+    # the device winner is the lexicographic min of the device keys ...
+    prio = np.array([ev.decode(s) is not None for s in [d.serial]])
+    assert prio.all()
+    order = np.lexsort((np.arange(n), keys[:, 1], keys[:, 0]))
+    # ... and nothing in the oracle sample beats it
+    best = (d.cost, d.finish, d.priority, d.serial)
+    for s, (oc, of) in zip(sample, r["keys"]):
+        assert best <= (oc, of, _prio(ev, s), s)
+    return d
+
+
+def _prio(ev, s):
+    from paper_2604_23838_b200.model import Exclusive, Merge
+
+    a = ev.decode(s)
+    return 1 if isinstance(a, Merge) else (2 if isinstance(a, Exclusive) else 0)
+
+
+def test_config4_livelock_matches_oracle(Evaluator):
+    """Both the device and the oracle raise on the same livelocking candidate."""
+    from oracle.oracle import Oracle, OracleError
+
+    inst = instance("config4")
+    st = HostState(inst)
+    ev = Evaluator(inst)
+    with pytest.raises(SchedulingError) as ei:
+        ev.decide(st, 3, 3, shard=(84807, 84808))
+    assert "did not converge" in str(ei.value)
+    with pytest.raises(OracleError):
+        Oracle(inst).score(st, 3, 3, serials=[84807])
+    # non-merge candidates of the same decision score normally
+    n_mux = ev.count(st, 3, 3)
+    ev.decide(st, 3, 3, shard=(0, 64), want_keys=True)
+    r = Oracle(inst).score(st, 3, 3, serials=list(range(0, 64, 7)), want_keys=True)
+    for i, s in enumerate(range(0, 64, 7)):
+        assert tuple(ev.keys[s]) == tuple(r["keys"][i])
+    assert n_mux == 523264
+
+
+@pytest.mark.parametrize("cfg,window,cap,n_sample", [
+    ("config2", 2, 3, 96), ("config2", 2, None, 24), ("config3", 3, 3, 24), ("config5", 4, 3, 6),
+])
+def test_first_decision_vs_oracle(Evaluator, cfg, window, cap, n_sample):
+    inst = instance(cfg)
+    ev = Evaluator(inst)
+    st = HostState(inst)
+    _oracle_sample_check(inst, st, window, cap, n_sample, ev)
+
+
+def test_config2_schedule_prefix_vs_oracle(Evaluator):
+    """Several consecutive decisions of config 2 (cap 3): each device winner
+    is re-derived on the oracle's full scoring of that decision."""
+    from oracle.oracle import Oracle
+
+    inst = instance("config2")
+    ev = Evaluator(inst)
+    o = Oracle(inst)
+    st = HostState(inst)
+    for _ in range(6):
+        d = ev.decide(st, 2, 3)
+        if d.n_candidates == 0:
+            st.advance()
+            continue
+        r = o.score(st, 2, 3)
+        assert r["best"] == (d.cost, d.finish, d.priority, d.serial)
+        st.apply(ev.decode(d.serial))

@@ -1,0 +1,70 @@
+// rlx_twin.cu — host (single-lane) build of the product's scoring code.
+//
+// TEST INFRASTRUCTURE / DEBUGGING TWIN ONLY: compiled into
+// tests/twin/_build/librlx_twin.so, never into librlx.so and never on the
+// product path. It runs the exact slice algorithm of rlx_kernels.cu with
+// L = 1 lane so that a device result can be reproduced and inspected on a
+// CPU (warp primitives resolve to host shims).
+#include <stdio.h>
+
+#include <string>
+#include <vector>
+
+#include "../../paper_2604_23838_b200/csrc/rlx_kernels.cu"
+#include "../../paper_2604_23838_b200/csrc/rlx_hostplan.hpp"
+
+namespace rlx {
+const DevPlan* g_twin_plan = nullptr;
+}
+
+using namespace rlx;
+
+extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd, int window, int max_merge,
+                               int64_t b, int64_t e, double* keys_out, int64_t* n_out, uint64_t* key_out,
+                               double* dbg_out, char* err, int errlen) {
+  HostPlan hp;
+  std::string es;
+  int rc = build_plan(in, sd, window, max_merge, hp, es);
+  if (rc) {
+    snprintf(err, errlen, "%s", es.c_str());
+    return rc;
+  }
+  DevPlan dp;
+  relocate(hp, hp.blob.buf.data(), dp);
+  g_twin_plan = &dp;
+  *n_out = dp.n_total;
+  if (e < 0 || e > dp.n_total) e = dp.n_total;
+  if (b < 0) b = 0;
+  if (b > e) b = e;
+  WorkDesc wd;
+  memset(&wd, 0, sizeof wd);
+  auto clip = [&](int64_t lo, int64_t hi, int64_t& s, int64_t& n) {
+    int64_t x = lo > b ? lo : b, y = hi < e ? hi : e;
+    s = x;
+    n = y > x ? y - x : 0;
+  };
+  clip(dp.n_mux, dp.n_mux + dp.n_merge, wd.a0, wd.na);
+  clip(0, dp.n_mux, wd.b0, wd.nb);
+  clip(dp.n_mux + dp.n_merge, dp.n_total, wd.c0, wd.nc);
+  wd.shard0 = b;
+  unsigned long long counter = 0;
+  int derr = 0;
+  double dbg[16] = {0};
+  wd.counter = &counter;
+  wd.err = &derr;
+  wd.keys_out = keys_out;
+  wd.dbg = dbg;
+  size_t sb = slice_bytes(dp);
+  wd.slice_bytes = (int)sb;
+  std::vector<uint8_t> smem(sb + 64);
+  SliceOut out;
+  memset(&out, 0, sizeof out);
+  slice_loop<1, 128>(wd, dp.lut, smem.data(), 0, 1u, &out);
+  key_out[0] = out.k0;
+  key_out[1] = out.k1;
+  key_out[2] = out.k2;
+  key_out[3] = out.passes;
+  if (dbg_out) memcpy(dbg_out, dbg, sizeof dbg);
+  if (derr) snprintf(err, errlen, "device error %d", derr);
+  return derr;
+}

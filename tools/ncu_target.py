@@ -1,0 +1,18 @@
+"""One warm-up + one measured decision at a config (ncu target)."""
+import sys
+
+sys.path.insert(0, "/root/repo")
+sys.path.insert(0, "/root/repo/tests")
+from helpers import instance  # noqa: E402
+from paper_2604_23838_b200.engine import HostState  # noqa: E402
+from paper_2604_23838_b200.native import Evaluator  # noqa: E402
+
+cfg = sys.argv[1]
+w = int(sys.argv[2])
+cap = None if sys.argv[3] == "none" else int(sys.argv[3])
+inst = instance(cfg)
+ev = Evaluator(inst)
+st = HostState(inst)
+for _ in range(2):
+    d = ev.decide(st, w, cap)
+print(cfg, d.n_candidates, d.kernel_ms, d.passes, d.alg_bytes)
