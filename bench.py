@@ -1,0 +1,377 @@
+"""Benchmark of the B200 look-ahead chooser (the north-star hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config config2] [--impl ours|reference]
+
+A *step* is one look-ahead decision: every candidate of the decision state
+(enumerate_actions, rlmux/scheduler.py:648-703) is scored by the W-round
+list-scheduling simulation (candidate_cost + action_finish_estimate,
+:773-918) and the (cost, finish, priority, serial) argmin is taken
+(:963-972). The workload is the FIRST decision of the named config
+(tests/golden/instances/<config>.json.gz, built with the reference's own
+generator), default config 2 = BASELINE.json configs[1]:
+2 multiplexed sync pipelines (8B + 14B), 16 simulated GPUs, 1,024
+rollouts, depth 2, long-tail migration on, uncapped merges -> 1,048,864
+candidates per decision.
+
+Reported (one JSON line on rank 0):
+  value      candidates evaluated / s, whole job, plan resident in HBM
+             (RLX_F_REUSE_PLAN: scoring kernel + argmin + cross-GPU min-loc),
+             CUDA events on the launching stream, max over ranks
+  e2e        the same metric through the public chooser (the `_drive` seam):
+             host state encode -> plan -> H2D -> kernel -> D2H -> action
+  roofline   SURVEY §8(d) algorithmic bytes of the scoring kernel per launch
+             / its CUDA-event duration, against the measured HBM copy peak
+  cpu_baseline  the CPU oracle port (oracle/rlx_oracle.c, all host threads)
+             on a bounded random sample of the same decision's candidates
+
+With N>1 (torchrun, NCCL) the global serial range is split into N
+contiguous shards and the shard winners meet in ONE all-reduce per
+decision (paper_2604_23838_b200/dist.py), i.e. weak-in-hardware,
+strong-in-work scaling ("strong": the decision is fixed).
+
+`--impl reference` times the reference algorithm on the host cores: the C
+restatement in oracle/ (the reference is pure Python and has no native
+build, so the port is the reference arm), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (window, max_merge, description)
+    "config1": (1, None, "sync GRPO, 1 Qwen3-8B-shaped pipeline, 8 simulated GPUs, 256 rollouts, depth 1"),
+    "config2": (2, None, "2 multiplexed sync pipelines (8B+14B), 16 simulated GPUs, 1024 rollouts, depth 2, "
+                         "long-tail migration, uncapped merges"),
+    "config3": (3, 3, "async RL 4 pipelines, 32 simulated GPUs, 4096 heavy-tailed rollouts, depth 3, merge cap 3"),
+    "config5": (4, 3, "8 pipelines, 64 simulated GPUs, 64k rollouts, depth 4, merge cap 3"),
+}
+METRIC = "look-ahead candidates evaluated/sec & p50 decision latency at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def load_instance(name):
+    from paper_2604_23838_b200 import load_instance as li
+
+    return li(os.path.join(ROOT, "tests", "golden", "instances", f"{name}.json.gz"))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config):
+    """dram read+write bytes per scoring launch from the committed ncu capture, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_sample(inst, state, window, cap, n_total, seconds, seed=0):
+    """Score a bounded uniform random sample of the decision's candidates on
+    the CPU oracle with every host thread; returns (cand/s, n, threads, s)."""
+    import numpy as np
+
+    from oracle.oracle import Oracle
+
+    threads = os.cpu_count() or 1
+    o = Oracle(inst, nthreads=threads)
+    rng = np.random.default_rng(seed)
+    # calibrate on one batch of `threads` candidates, then size the sample
+    first = rng.choice(n_total, size=min(threads, n_total), replace=False)
+    t = time.perf_counter()
+    o.score(state, window, cap, serials=np.sort(first), want_keys=True)
+    dt = time.perf_counter() - t
+    per_batch = max(dt, 1e-6)
+    batches = max(1, min(int(seconds / per_batch), 10_000 // threads))
+    n = min(batches * threads, n_total)
+    sample = np.sort(rng.choice(n_total, size=n, replace=False))
+    t = time.perf_counter()
+    o.score(state, window, cap, serials=sample, want_keys=True)
+    dt = time.perf_counter() - t
+    return n / dt, n, threads, dt
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2604_23838_b200.engine import HostState
+
+    window, cap, desc = CONFIGS[args.config]
+    inst = load_instance(args.config)
+    st = HostState(inst)
+    from oracle.oracle import Oracle
+
+    n_total = Oracle(inst, nthreads=1).score(st, window, cap, serials=[])["n"]
+    rates = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds / max(args.steps, 1), seed=i)
+        if i >= args.warmup:
+            rates.append(r)
+        last = r
+    tot_n = sum(r[1] for r in rates)
+    tot_s = sum(r[3] for r in rates)
+    value = tot_n / tot_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / len(rates),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator, golden instance)",
+        "config": {"workload": f"{args.config} first decision: {desc}", "window": window, "max_merge": cap,
+                   "candidates_per_decision": n_total},
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": last[2], "kind": "port",
+                         "sample": f"{last[1]} uniformly sampled candidates of the {n_total}-candidate decision "
+                                   f"per step, scored by oracle/rlx_oracle.c on {last[2]} threads ({cpu_model()})"},
+        "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2604_23838_b200.dist import WORDS, best_row, unpack
+    from paper_2604_23838_b200.engine import HostState
+    from paper_2604_23838_b200.native import Evaluator
+
+    window, cap, desc = CONFIGS[args.config]
+    inst = load_instance(args.config)
+    st = HostState(inst)
+    ev = Evaluator(inst, device=local)
+    stream = torch.cuda.current_stream(dev)
+    ev.set_stream(stream.cuda_stream)
+    part = (rank, world)
+    table = torch.zeros((world, WORDS), dtype=torch.int64, device=dev)
+    row_ptr = table.data_ptr() + rank * WORDS * 8
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def minloc():
+        if world > 1:
+            dist.all_reduce(table, op=dist.ReduceOp.SUM)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- plan + upload once (also the first warm-up), then the resident loop
+    d0 = ev.decide(st, window, cap, part=part, dev_key_ptr=row_ptr)
+    n_total = d0.n_candidates
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kern_ms, bytes_l, passes_l = [], [], []
+    winners = set()
+    for i in range(args.warmup):
+        table.zero_()
+        ev.rescore(window, part=part, dev_key_ptr=row_ptr)
+        minloc()
+    torch.cuda.synchronize(dev)
+    barrier()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(i)  # L2 flush between timed steps (outside the step events)
+            table.zero_()
+            ev_a[i].record(stream)
+            d = ev.rescore(window, part=part, dev_key_ptr=row_ptr)
+            minloc()
+            ev_b[i].record(stream)
+            kern_ms.append(d.kernel_ms)
+            bytes_l.append(d.alg_bytes)
+            passes_l.append(d.passes)
+            rows = table.cpu().numpy().view(np.uint64)
+            winners.add(unpack(rows[best_row(rows)]))
+        torch.cuda.synchronize(dev)
+        barrier()
+        step_ms = [a.elapsed_time(bb) for a, bb in zip(ev_a, ev_b)]
+        # ---- e2e through the public chooser (host state in, action out)
+        choose = ev.chooser(window, cap, group=dist.group.WORLD if world > 1 else None)
+        e2e_ms, wall_ms = [], []
+        e2e_steps = max(args.steps, 3)
+        for i in range(args.warmup + e2e_steps):
+            flush.fill_(i)
+            torch.cuda.synchronize(dev)
+            barrier()
+            t = time.perf_counter()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            action = choose(st)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            w = (time.perf_counter() - t) * 1e3
+            if i >= args.warmup:
+                e2e_ms.append(a0.elapsed_time(a1))
+                wall_ms.append(w)
+        last_e2e = ev.last
+    clocks = clk.summary()
+    sum_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = sum_ms / args.steps
+    e2e_sum = max_over_ranks(sum(e2e_ms))
+    p50_wall = max_over_ranks(statistics.median(wall_ms))
+    kernel_avg = max_over_ranks(sum(kern_ms) / len(kern_ms))
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+    value = n_total * args.steps / (sum_ms / 1e3)
+    e2e_value = n_total * len(e2e_ms) / (e2e_sum / 1e3)
+    peak, peak_src = measured_peak()
+    alg_bytes = statistics.mean(bytes_l)  # rank 0's shard bytes per launch
+    achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
+    traffic = ncu_traffic(args.config)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, n, threads, secs = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "candidates/s", "cores": threads, "kind": "port",
+               "sample": f"{n} uniformly sampled candidates of the {n_total}-candidate decision, scored by "
+                         f"oracle/rlx_oracle.c on {threads} host threads in {secs:.1f} s ({cpu_model()})"}
+    winner = sorted(winners)
+    line = {
+        "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, golden instance)",
+        "config": {"workload": f"{args.config} first decision: {desc}", "window": window, "max_merge": cap,
+                   "candidates_per_decision": n_total, "parallelism": f"candidate shards x{world}",
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)"},
+        "decisions_per_s": 1e3 / ms_per_step,
+        "p50_decision_ms": p50_wall,
+        "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": int(last_e2e.h2d_bytes),
+                "d2h_bytes_per_step": int(last_e2e.d2h_bytes) + (8 * WORDS * world if world > 1 else 0),
+                "p50_decision_ms": p50_wall, "decisions_per_s": 1e3 * len(e2e_ms) / e2e_sum},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "rlx_score_kernel",
+                     "kernel_ms": statistics.mean(kern_ms), "alg_bytes_per_launch": alg_bytes,
+                     "passes_per_launch": statistics.mean(passes_l),
+                     "kernel_share_of_step": kernel_avg / ms_per_step},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+        "winner": {"cost": winner[0][0], "finish": winner[0][1], "priority": winner[0][2],
+                   "serial": winner[0][3]} if len(winner) == 1 else [list(w) for w in winner],
+        "first_decide_plan_ms": d0.plan_ms,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("RLX_BENCH_CONFIG", "config2"), choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

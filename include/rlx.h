@@ -15,6 +15,7 @@
  *                                  serial range (replaces scheduler.py:939-940 and :963-972)
  *   rlx_decode                     serial -> action (so every rank can materialise the
  *                                  global winner after the cross-GPU min-loc)
+ *   rlx_set_stream                 order the handle's work on a caller stream
  *   rlx_last_error                 text of the last failure
  *
  * All arrays are plain host pointers owned by the caller and only read
@@ -30,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RLX_ABI_VERSION 1
+#define RLX_ABI_VERSION 2
 
 /* Kind codes = declaration order of rlmux SubStageKind (graph.py:69-76). */
 enum {
@@ -144,6 +145,11 @@ typedef struct RlxDecideArgs {
 } RlxDecideArgs;
 
 #define RLX_F_NO_SYNC_STATS 1     /* skip the stats readback */
+#define RLX_F_REUSE_PLAN 2        /* re-score the plan already resident on the device   */
+                                  /*   (state may be NULL; no planning, no H2D copy)     */
+#define RLX_F_SHARD 4             /* serial_begin/serial_end = shard index / shard count: */
+                                  /*   score the contiguous block [r*q+min(r,m), ...) of  */
+                                  /*   n = q*count+m serials (dist.shard_range)           */
 
 /* Packed key: cost and finish are non-negative doubles, so their bit
  * patterns order as uint64; word 2 = priority << 61 | serial; word 3 = 1 if
@@ -181,6 +187,10 @@ typedef struct RlxDecision {
   double kernel_ms;              /* device time of the scoring kernel (CUDA events)       */
   double plan_ms;                /* host planning time                                    */
   int64_t n_merge, n_multiplex, n_exclusive;
+  double device_ms;              /* device time from plan upload to the reduced key       */
+  int64_t h2d_bytes;             /* plan bytes copied host -> device by this call         */
+  int64_t d2h_bytes;             /* result bytes copied device -> host                    */
+  int64_t shard_begin, shard_end;/* serial range actually scored                          */
 } RlxDecision;
 
 int rlx_abi_version(void);
@@ -188,6 +198,11 @@ int rlx_open(int device, void** handle);
 int rlx_load_instance(void* handle, const RlxInstanceDesc* inst);
 int rlx_decide(void* handle, const RlxStateDesc* state, const RlxDecideArgs* args, RlxDecision* out);
 int rlx_decode(void* handle, int64_t serial, RlxAction* out);
+/* Issue all further work of this handle on `cuda_stream` (a cudaStream_t of
+ * the handle's device, e.g. the caller's current torch stream, so CUDA
+ * events and NCCL calls on that stream order with the scoring kernel);
+ * NULL restores the handle's private stream. */
+int rlx_set_stream(void* handle, void* cuda_stream);
 const char* rlx_last_error(void* handle);
 void rlx_close(void* handle);
 

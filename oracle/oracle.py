@@ -61,6 +61,10 @@ class Oracle:
 
     def score(self, state, window: int, max_merge: int | None = None, serials=None, want_keys=False):
         """Returns dict(n, best=(cost, finish, prio, serial) or None, keys=ndarray[k,2] or None)."""
+        n_all = None
+        if want_keys and serials is None:
+            # the count first: every encode() replaces the arrays an earlier descriptor points into
+            n_all = self.score(state, window, max_merge, serials=[], want_keys=False)["n"]
         sd = self.senc.encode(state)
         mm = 0 if max_merge is None else int(max_merge)
         ser = None
@@ -74,9 +78,7 @@ class Oracle:
         if want_keys:
             n_hint = nser if serials is not None else None
             if n_hint is None:
-                # need the count first
-                info = self.score(state, window, max_merge, serials=[], want_keys=False)
-                n_hint = info["n"]
+                n_hint = n_all
             keys = np.zeros((max(n_hint, 1), 2), dtype=np.float64)
             kp = keys.ctypes.data_as(C.POINTER(C.c_double))
         if serials is not None and nser == 0:

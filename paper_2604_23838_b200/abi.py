@@ -4,7 +4,10 @@ from __future__ import annotations
 
 import ctypes as C
 
-RLX_ABI_VERSION = 1
+RLX_ABI_VERSION = 2
+RLX_F_NO_SYNC_STATS = 1
+RLX_F_REUSE_PLAN = 2
+RLX_F_SHARD = 4
 RLX_NKIND = 7
 RLX_NALLOC = 25
 RLX_NPARTNER = 8
@@ -72,12 +75,14 @@ class RlxDecision(C.Structure):
         ("cost", C.c_double), ("finish", C.c_double), ("action", RlxAction), ("key", RlxKey),
         ("passes", C.c_int64), ("alg_bytes", C.c_double), ("kernel_ms", C.c_double), ("plan_ms", C.c_double),
         ("n_merge", C.c_int64), ("n_multiplex", C.c_int64), ("n_exclusive", C.c_int64),
+        ("device_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+        ("shard_begin", C.c_int64), ("shard_end", C.c_int64),
     ]
 
 
 # Every symbol include/rlx.h declares (checked by tests/test_abi.py).
 EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "rlx_decode",
-            "rlx_last_error", "rlx_close")
+            "rlx_last_error", "rlx_close", "rlx_set_stream")
 
 
 def bind(lib: C.CDLL) -> C.CDLL:
@@ -94,6 +99,8 @@ def bind(lib: C.CDLL) -> C.CDLL:
     lib.rlx_decode.argtypes = [C.c_void_p, C.c_int64, C.POINTER(RlxAction)]
     lib.rlx_last_error.restype = C.c_char_p
     lib.rlx_last_error.argtypes = [C.c_void_p]
+    lib.rlx_set_stream.restype = C.c_int
+    lib.rlx_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     lib.rlx_close.restype = None
     lib.rlx_close.argtypes = [C.c_void_p]
     return lib

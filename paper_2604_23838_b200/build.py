@@ -16,6 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librlx.so")
+LIB_DBG = os.path.join(HERE, "librlx_dbg.so")
 SOURCES = ("rlx_abi.cu", "rlx_kernels.cu", "rlx_plan.cpp")
 HEADERS = ("rlx_plan.hpp", "rlx_hostplan.hpp")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
@@ -28,32 +29,38 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = None) -> bool:
+    lib = lib or LIB
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "rlx.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False) -> str:
+    """Compile librlx.so (or, with debug_shapes, the development variant
+    librlx_dbg.so whose lane shape can be forced with RLX_SHAPE=L,WPL)."""
+    lib = LIB_DBG if debug_shapes else LIB
+    if not force and not _stale(lib):
+        return lib
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
+        obj = os.path.join(CSRC, src + (".dbg.o" if debug_shapes else ".o"))
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "-c", os.path.join(CSRC, src), "-o", obj]
+        if debug_shapes:
+            cmd.insert(1, "-DRLX_DEBUG_SHAPES")
         if verbose and src.endswith("kernels.cu"):
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc(), ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    print(build(force=True, verbose="--verbose" in sys.argv, debug_shapes="--debug-shapes" in sys.argv))

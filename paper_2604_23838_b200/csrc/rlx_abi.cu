@@ -28,8 +28,9 @@ constexpr size_t kSliceOutBytes = 48;
 struct Handle {
   int device = 0;
   int sm_count = 148;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaStream_t stream = nullptr;      // stream every call is issued on
+  cudaStream_t own_stream = nullptr;  // the handle's private stream (default)
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
   std::string err;
   // owned instance copy
   bool loaded = false;
@@ -97,8 +98,9 @@ int rlx_open(int device, void** handle) {
     return RLX_ERR_CUDA;
   }
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&h->e0) != cudaSuccess || cudaEventCreate(&h->e1) != cudaSuccess ||
+      cudaEventCreate(&h->e2) != cudaSuccess ||
       cudaMalloc(&h->d_outs, kSliceOutBytes * kMaxSlices) != cudaSuccess ||
       cudaMalloc(&h->d_counter, 64) != cudaSuccess || cudaMalloc(&h->d_err, 64) != cudaSuccess ||
       cudaMalloc(&h->d_res, 64) != cudaSuccess || cudaMallocHost(&h->h_res, 64) != cudaSuccess ||
@@ -106,6 +108,7 @@ int rlx_open(int device, void** handle) {
     delete h;
     return RLX_ERR_CUDA;
   }
+  h->stream = h->own_stream;
   const char* th = getenv("RLX_THREADS");
   if (th) h->threads_hint = atoi(th);
   *handle = h;
@@ -174,18 +177,24 @@ static void fill_action(Handle* h, const Cand& c, RlxAction* out) {
 
 int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, RlxDecision* out) {
   Handle* h = (Handle*)handle;
-  if (!h || !sd || !args || !out) return RLX_ERR_ARG;
+  if (!h || !args || !out) return RLX_ERR_ARG;
   if (!h->loaded) return fail(h, RLX_ERR_ARG, "no instance loaded");
   if (args->window < 1) return fail(h, RLX_ERR_VALUE, "window must be >= 1");
+  const bool reuse = (args->flags & RLX_F_REUSE_PLAN) != 0;
+  if (reuse && !h->have_plan) return fail(h, RLX_ERR_ARG, "RLX_F_REUSE_PLAN needs a preceding rlx_decide");
+  if (!reuse && !sd) return RLX_ERR_ARG;
   memset(out, 0, sizeof *out);
   out->serial = -1;
   CK(cudaSetDevice(h->device));
   auto t0 = std::chrono::steady_clock::now();
-  h->have_plan = false;
-  int rc = build_plan(&h->inst, sd, args->window, args->max_merge, h->hp, h->err);
-  if (rc) return rc;
-  h->have_plan = true;
-  relocate(h->hp, h->hp.blob.buf.data(), h->host_view);
+  int rc = 0;
+  if (!reuse) {
+    h->have_plan = false;
+    rc = build_plan(&h->inst, sd, args->window, args->max_merge, h->hp, h->err);
+    if (rc) return rc;
+    h->have_plan = true;
+    relocate(h->hp, h->hp.blob.buf.data(), h->host_view);
+  }
   const DevPlan& hv = h->host_view;
   out->n_candidates = hv.n_total;
   out->n_merge = hv.n_merge;
@@ -193,6 +202,15 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   out->n_exclusive = hv.n_excl;
   int64_t b = args->serial_begin < 0 ? 0 : args->serial_begin;
   int64_t e = args->serial_end < 0 ? hv.n_total : args->serial_end;
+  if (args->flags & RLX_F_SHARD) {  // contiguous block `serial_begin` of `serial_end` blocks
+    const int64_t r = args->serial_begin, w = args->serial_end;
+    if (w < 1 || r < 0 || r >= w) return fail(h, RLX_ERR_ARG, "bad shard index / count");
+    const int64_t q = hv.n_total / w, rem = hv.n_total % w;
+    b = r * q + (r < rem ? r : rem);
+    e = b + q + (r < rem ? 1 : 0);
+  }
+  out->shard_begin = b;
+  out->shard_end = e;
   if (e > hv.n_total) e = hv.n_total;
   if (b > e) b = e;
   auto t1 = std::chrono::steady_clock::now();
@@ -205,9 +223,12 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
     }
     return RLX_OK;
   }
-  // ---- upload plan
+  // ---- upload plan (skipped when re-scoring the resident plan)
   size_t nb = h->hp.blob.buf.size();
-  if (nb > h->pin_cap) {
+  CK(cudaEventRecord(h->e2, h->stream));
+  if (reuse) {
+    nb = 0;
+  } else if (nb > h->pin_cap) {
     if (h->h_pin) cudaFreeHost(h->h_pin);
     h->pin_cap = nb * 2;
     CK(cudaMallocHost(&h->h_pin, h->pin_cap));
@@ -217,8 +238,11 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
     h->blob_cap = nb * 2;
     CK(cudaMalloc(&h->d_blob, h->blob_cap));
   }
-  memcpy(h->h_pin, h->hp.blob.buf.data(), nb);
-  CK(cudaMemcpyAsync(h->d_blob, h->h_pin, nb, cudaMemcpyHostToDevice, h->stream));
+  if (nb) {
+    memcpy(h->h_pin, h->hp.blob.buf.data(), nb);
+    CK(cudaMemcpyAsync(h->d_blob, h->h_pin, nb, cudaMemcpyHostToDevice, h->stream));
+  }
+  out->h2d_bytes = (int64_t)nb;
   DevPlan dp;
   relocate(h->hp, h->d_blob, dp);
   // ---- work ranges: merges first (heaviest), then multiplex, then exclusive
@@ -265,6 +289,9 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->e0, h->e1);
   out->kernel_ms = ms;
+  cudaEventElapsedTime(&ms, h->e2, h->e1);
+  out->device_ms = ms;
+  out->d2h_bytes = 60;
   if (herr) {
     if (herr == RLX_ERR_SCHEDULING) {
       cudaMemcpy(h->h_dbg, h->d_dbg, sizeof h->h_dbg, cudaMemcpyDeviceToHost);
@@ -303,6 +330,13 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   return RLX_OK;
 }
 
+int rlx_set_stream(void* handle, void* stream) {
+  Handle* h = (Handle*)handle;
+  if (!h) return RLX_ERR_ARG;
+  h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+  return RLX_OK;
+}
+
 int rlx_decode(void* handle, int64_t serial, RlxAction* out) {
   Handle* h = (Handle*)handle;
   if (!h || !out) return RLX_ERR_ARG;
@@ -333,7 +367,8 @@ void rlx_close(void* handle) {
   if (h->d_dbg) cudaFree(h->d_dbg);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->e2) cudaEventDestroy(h->e2);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
 

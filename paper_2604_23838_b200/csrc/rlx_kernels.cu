@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/rlx.h"
@@ -883,6 +885,12 @@ static KernelFn pick(int L, int WPL) {
 #ifdef RLX_ONLY_32_2
   return rlx_score_kernel<32, 2>;
 #endif
+#ifdef RLX_DEBUG_SHAPES
+  // development builds only (librlx_dbg.so): lane-count sweeps for bisecting
+  if (L == 4 && WPL == 8) return rlx_score_kernel<4, 8>;
+  if (L == 8 && WPL == 4) return rlx_score_kernel<8, 4>;
+  if (L == 16 && WPL == 2) return rlx_score_kernel<16, 2>;
+#endif
   if (L == 4) return rlx_score_kernel<4, 1>;
   if (L == 8) return rlx_score_kernel<8, 1>;
   if (L == 16) return rlx_score_kernel<16, 1>;
@@ -905,6 +913,9 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
                  int* n_slices_out, int threads_hint) {
   int L, WPL;
   choose_shape(P.W, L, WPL);
+#ifdef RLX_DEBUG_SHAPES
+  if (const char* sh = getenv("RLX_SHAPE")) sscanf(sh, "%d,%d", &L, &WPL);
+#endif
   KernelFn fn = pick(L, WPL);
   size_t sb = slice_bytes(P);
   wd.slice_bytes = (int)sb;

@@ -41,6 +41,16 @@ def best_row(rows: np.ndarray) -> int:
     return best
 
 
+def pack(cost: float, finish: float, priority: int, serial: int) -> np.ndarray:
+    """(cost, finish, priority, serial) -> the 4-word key of include/rlx.h
+    RlxKey (costs are >= 0 doubles, so their bit patterns order as u64)."""
+    w = np.zeros(WORDS, dtype=np.uint64)
+    w[0:2] = np.array([cost + 0.0, finish + 0.0], dtype=np.float64).view(np.uint64)
+    w[2] = (int(priority) << 61) | int(serial)
+    w[3] = 1
+    return w
+
+
 def unpack(row) -> tuple:
     """(cost, finish, priority, serial) of a packed key row."""
     w = np.asarray(row, dtype=np.uint64)
@@ -79,14 +89,15 @@ class ShardedChooser:
 
     def __call__(self, state):
         ev = self.ev
-        n = ev.count(state, self.window, self.max_merge)
-        if n == 0:
-            return None
-        b, e = shard_range(n, self.rank, self.world)
         self.table.zero_()
         self.torch.cuda.synchronize(self.table.device)
         row_ptr = self.table.data_ptr() + self.rank * WORDS * 8
-        ev.decide(state, self.window, self.max_merge, shard=(b, e), dev_key_ptr=row_ptr)
+        # one plan per decision: the library sizes block `rank` of `world`
+        # from the candidate count it enumerates (same as shard_range)
+        d = ev.decide(state, self.window, self.max_merge, part=(self.rank, self.world), dev_key_ptr=row_ptr)
+        n = d.n_candidates
+        if n == 0:
+            return None
         rows = minloc_allreduce(self.table, self.rank, self.group)
         i = best_row(rows)
         cost, fin, prio, serial = unpack(rows[i])

@@ -223,6 +223,12 @@ class StateEncoding:
         d.grant_worker = _ptr(self.grant_worker, C.c_int32)
         d.grant_pipe = _ptr(self.grant_pipe, C.c_int32)
         d.grant_mem = _ptr(self.grant_mem, C.c_double)
+        # the descriptor owns the arrays it points into, so it stays valid
+        # after a later encode() rebinds the attributes above
+        d._keep = (self.pipe, self.worker, self.kind, self.duration, self.mem, self.remaining, self.active,
+                   self.context, self.completed, self.merge_prefix, self._ids, self.id_off, self.edge_src,
+                   self.edge_dst, self.run_node, self.run_partner, self.run_rate, self.run_prefix, self.run_work,
+                   self.tw_node, self.tw_end, self.grant_worker, self.grant_pipe, self.grant_mem)
         self.desc = d
         return d
 

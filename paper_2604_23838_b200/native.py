@@ -18,7 +18,7 @@ from .encode import InstanceEncoding, StateEncoding
 from .model import SchedulingError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librlx.so")
+LIB_PATH = os.environ.get("RLX_LIB") or os.path.join(HERE, "librlx.so")
 _lib = None
 
 
@@ -88,16 +88,26 @@ class Evaluator:
             pass
 
     def decide(self, state, window: int, max_merge: int | None = None, shard=None, want_keys=False,
-               dev_key_ptr: int | None = None) -> abi.RlxDecision:
-        """Score every candidate of `state` (or the serial shard [b, e)) on the GPU."""
+               dev_key_ptr: int | None = None, part=None) -> abi.RlxDecision:
+        """Score every candidate of `state` on the GPU — or the serial shard
+        [b, e) (`shard`), or contiguous block r of w (`part=(r, w)`, sized by
+        the library from the candidate count, dist.shard_range)."""
+        n_all = self.count(state, window, max_merge) if (want_keys and shard is None) else None
+        # encode AFTER count(): every encode() replaces the arrays the previous
+        # descriptor points into
         sd = self.senc.encode(state)
         args = abi.RlxDecideArgs()
         args.window = int(window)
         args.max_merge = 0 if max_merge is None else int(max_merge)
         args.serial_begin, args.serial_end = (0, -1) if shard is None else (int(shard[0]), int(shard[1]))
+        if part is not None:
+            if want_keys:
+                raise ValueError("want_keys needs an explicit shard")
+            args.serial_begin, args.serial_end = int(part[0]), int(part[1])
+            args.flags |= abi.RLX_F_SHARD
         keys = None
         if want_keys:
-            n = self.count(state, window, max_merge) if shard is None else shard[1] - shard[0]
+            n = n_all if shard is None else shard[1] - shard[0]
             keys = np.zeros((max(int(n), 1), 2), dtype=np.float64)
             args.keys_out = keys.ctypes.data_as(C.POINTER(C.c_double))
         args.dev_key_out = dev_key_ptr
@@ -112,6 +122,31 @@ class Evaluator:
             nk = out.n_candidates if shard is None else min(shard[1], out.n_candidates) - shard[0]
             self.keys = keys[: max(int(nk), 0)]
         return out
+
+    def rescore(self, window: int, shard=None, dev_key_ptr: int | None = None, part=None) -> abi.RlxDecision:
+        """Re-run scoring + argmin on the plan already resident on the device
+        (RLX_F_REUSE_PLAN): the device-only part of the last `decide`."""
+        args = abi.RlxDecideArgs()
+        args.window = int(window)
+        args.serial_begin, args.serial_end = (0, -1) if shard is None else (int(shard[0]), int(shard[1]))
+        args.dev_key_out = dev_key_ptr
+        args.flags = abi.RLX_F_REUSE_PLAN
+        if part is not None:
+            args.serial_begin, args.serial_end = int(part[0]), int(part[1])
+            args.flags |= abi.RLX_F_SHARD
+        out = abi.RlxDecision()
+        rc = self.lib.rlx_decide(self.handle, None, C.byref(args), C.byref(out))
+        if rc != 0:
+            _raise(rc, self.error())
+        self.last = out
+        return out
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        """Issue the handle's work on a caller CUDA stream (e.g. torch's
+        current stream, so torch CUDA events and NCCL order with it)."""
+        rc = self.lib.rlx_set_stream(self.handle, stream_ptr or None)
+        if rc != 0:
+            _raise(rc, self.error())
 
     def count(self, state, window: int, max_merge: int | None = None) -> int:
         """Candidate count of a state (planning only: an empty shard)."""
