@@ -22,7 +22,7 @@ using namespace rlx;
 
 namespace {
 
-constexpr int kMaxSlices = 1 << 16;
+constexpr int kMaxSlices = 1 << 17;
 constexpr size_t kSliceOutBytes = 48;
 
 struct Handle {
@@ -269,9 +269,10 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
     wd.keys_out = h->d_keys;
   }
   CK(cudaMemsetAsync(h->d_counter, 0, 8, h->stream));
-  CK(cudaMemsetAsync(h->d_err, 0, 4, h->stream));
+  CK(cudaMemsetAsync(h->d_err, 0, 32, h->stream));
   CK(cudaMemsetAsync(h->d_dbg, 0, 16 * sizeof(double), h->stream));
   wd.dbg = h->d_dbg;
+  wd.dbg_flag = h->d_err + 4;
   int n_slices = 0;
   CK(cudaEventRecord(h->e0, h->stream));
   rc = launch_score(dp, wd, (SliceOut*)h->d_outs, kMaxSlices, h->sm_count, h->stream, &n_slices, h->threads_hint);
@@ -298,9 +299,9 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
       char buf[400];
       snprintf(buf, sizeof buf,
                "window estimate did not converge (serial %.0f variant %.0f now %.17g done %.0f/%.0f tw_run %.0f "
-               "tw_live %.0f twq %.0f nm0 %.0f act %.0f/%.0f mt %.0f)",
-               h->h_dbg[1], h->h_dbg[2], h->h_dbg[3], h->h_dbg[4], h->h_dbg[5], h->h_dbg[6], h->h_dbg[7],
-               h->h_dbg[8], h->h_dbg[9], h->h_dbg[10], h->h_dbg[11], h->h_dbg[12]);
+               "act %.0f/%.0f mt %.0f)",
+               h->h_dbg[1], h->h_dbg[2], h->h_dbg[3], h->h_dbg[4], h->h_dbg[5], h->h_dbg[6], h->h_dbg[10],
+               h->h_dbg[11], h->h_dbg[12]);
       return fail(h, herr, buf);
     }
     if (herr == RLX_ERR_KEY) return fail(h, herr, "slowdown table or latency model has no entry for a queried pair");

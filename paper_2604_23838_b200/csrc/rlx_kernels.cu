@@ -1,27 +1,37 @@
-// rlx_kernels.cu — sm_100a look-ahead scoring kernel.
+// rlx_kernels.cu — sm_100a look-ahead evaluator.
 //
-// One "slice" of L lanes (L = 4..32, a warp or a fraction of one) runs one
-// list-scheduling pass (rlmux/scheduler.py:831-869) at a time; lane l owns
-// workers {l, l+L, ...}. Per pass, the slice's private shared memory holds
-// the pending-predecessor counters of every window node and one 64-bit
-// ready mask per worker whose bit order is that worker's completion-key
-// order (suffix key or name key, :893-894), so "first ready node on an
-// idle worker" is a find-first-set and the pairing partner is the next set
-// bit of another pipeline. Running members (<= 2 per worker) stay in the
-// owner lane's registers. Each event is: selection on idle workers ->
-// warp-shuffle min of finish estimates (the next event) -> consume ->
-// completions (smem atomics on counters / masks) -> tool-wait expiry and
-// auto-start -> window-completion count (__reduce_add_sync).
+// What one launch computes: for every candidate of a decision shard
+// (enumerate_actions, rlmux/scheduler.py:648-703) its look-ahead cost
+// (candidate_cost :902-918 = min over window_cost passes :878-899 of the
+// list-scheduling simulation _complete_window :831-869) and its finish
+// estimate (action_finish_estimate :773-789), then the lexicographic
+// (cost, finish, priority, serial) minimum (chooser :963-972).
 //
-// A persistent grid of slices pulls candidates from a global counter,
-// heaviest class first (merges carry 3*(1+F) passes, :902-918). For each
-// candidate the slice runs every pass, forms the key (cost, finish,
-// priority, serial) (:963-972) and keeps its running minimum; a final
-// reduction produces the shard winner.
+// Execution model (B200):
+//  * One persistent CTA per SM. Its first act is to stage the decision plan's
+//    hot region (node SoA, successor CSR, per-worker ready orders, slowdown
+//    LUT — everything the event loop reads) from HBM into shared memory with
+//    TMA bulk copies (cp.async.bulk + mbarrier complete_tx). All passes of all
+//    candidates on that SM then read the plan from shared memory only.
+//  * A "group" of G lanes (G = 1..16, inside one warp) runs one list-
+//    scheduling pass at a time. Lane l owns the simulated workers
+//    {l, l+G, ...} (WPL = workers per lane) and keeps their running members
+//    (<= 2 per worker: node, rate, work left) in registers; prefixes, ready
+//    masks, readiness counters and tool-wait clocks live in the group's slice
+//    of shared memory.
+//  * One loop iteration = one simulated event for every group of the warp:
+//    selection on idle workers (find-first-set over a 64-bit ready mask whose
+//    bit order is the completion key), group min of finish estimates
+//    (butterfly shuffles over G lanes), consume, completions (shared-memory
+//    atomics when G > 1), tool-wait expiry/auto-start, window count. The
+//    finish estimate of every member is produced in the same sweep that
+//    consumes it, so each event touches each member once.
+//  * Groups pull whole candidates from a global counter, heaviest class
+//    (merges: 3*(1+F) passes) first, and keep a running minimum key.
 //
-// Bit-exactness: compiled with -fmad=false; all double expressions keep
-// the reference's left-to-right order (e.g. finish = (now + prefix) +
-// work*rate, :328).
+// Bit-exactness: compiled with -fmad=false; every double expression keeps
+// the reference's left-to-right order (finish = (now + prefix) + work*rate,
+// :328; consume :330-336; re-rated pair end :792-800).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -29,19 +39,18 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "../../include/rlx.h"
 #include "rlx_plan.hpp"
 
 namespace rlx {
 
-constexpr int kLutN = RLX_NKIND * RLX_NPARTNER * RLX_NALLOC;
-// The decision plan lives in constant memory: every field is a uniform,
-// broadcast read for all lanes (one plan per device at a time).
+// Scalars and global views of the plan; uniform reads for every lane.
 __constant__ DevPlan c_plan;
 
-// The same slice code also compiles for the host as a single-lane debugging
-// twin (tests/twin, never linked into the product): PLAN and the warp
-// primitives resolve to their host equivalents there.
+// The same code compiles for the host as a single-lane debugging twin
+// (tests/twin, never linked into the product).
 #ifdef __CUDA_ARCH__
 #define PLAN c_plan
 #else
@@ -49,78 +58,91 @@ extern const DevPlan* g_twin_plan;
 #define PLAN (*g_twin_plan)
 #endif
 
+// ---------------------------------------------------------------------------
+// warp / atomic shims. With G == 1 a group is one lane and nothing is shared.
+template <int G>
 RLX_HD unsigned at_sub(unsigned* p, unsigned v) {
 #ifdef __CUDA_ARCH__
-  return atomicSub(p, v);
-#else
-  unsigned o = *p; *p = o - v; return o;
+  if (G > 1) return atomicSub(p, v);
 #endif
+  unsigned o = *p;
+  *p = o - v;
+  return o;
 }
+template <int G>
 RLX_HD int at_add(int* p, int v) {
 #ifdef __CUDA_ARCH__
-  return atomicAdd(p, v);
-#else
-  int o = *p; *p = o + v; return o;
+  if (G > 1) return atomicAdd(p, v);
 #endif
+  int o = *p;
+  *p = o + v;
+  return o;
 }
+template <int G>
 RLX_HD void at_or(unsigned long long* p, unsigned long long v) {
 #ifdef __CUDA_ARCH__
-  atomicOr(p, v);
-#else
-  *p |= v;
+  if (G > 1) {
+    atomicOr(p, v);
+    return;
+  }
 #endif
+  *p |= v;
 }
 RLX_HD unsigned long long at_add64(unsigned long long* p, unsigned long long v) {
 #ifdef __CUDA_ARCH__
   return atomicAdd(p, v);
 #else
-  unsigned long long o = *p; *p = o + v; return o;
+  unsigned long long o = *p;
+  *p = o + v;
+  return o;
 #endif
 }
 RLX_HD int at_cas(int* p, int c, int v) {
 #ifdef __CUDA_ARCH__
   return atomicCAS(p, c, v);
 #else
-  int o = *p; if (o == c) *p = v; return o;
+  int o = *p;
+  if (o == c) *p = v;
+  return o;
 #endif
 }
-RLX_HD void wsync(unsigned m) {
+template <int G>
+RLX_HD void gsync(unsigned m) {
 #ifdef __CUDA_ARCH__
-  __syncwarp(m);
+  if (G > 1) __syncwarp(m);
 #endif
 }
-RLX_HD bool wany(unsigned m, bool x) {
+template <int G>
+RLX_HD bool gany(unsigned m, bool x) {
 #ifdef __CUDA_ARCH__
-  return __any_sync(m, x);
-#else
+  if (G > 1) return __any_sync(m, x);
+#endif
   return x;
-#endif
 }
-RLX_HD unsigned wsum(unsigned m, unsigned x) {
+template <int G>
+RLX_HD unsigned gsum(unsigned m, unsigned x) {
 #ifdef __CUDA_ARCH__
-  return __reduce_add_sync(m, x);
-#else
-  return x;
+  if (G > 1) return __reduce_add_sync(m, x);
 #endif
+  return x;
 }
-template <int L>
-RLX_HD double wmin(unsigned m, double t) {
+template <int G>
+RLX_HD double gmin(unsigned m, double t) {
 #ifdef __CUDA_ARCH__
 #pragma unroll
-  for (int off = L / 2; off > 0; off >>= 1) {
-    double u = __shfl_xor_sync(m, t, off, L);
+  for (int off = G / 2; off > 0; off >>= 1) {
+    double u = __shfl_xor_sync(m, t, off, G);
     t = u < t ? u : t;
   }
 #endif
   return t;
 }
-template <int L>
-RLX_HD long long wbcast(unsigned m, long long v) {
+template <int G>
+RLX_HD long long gbcast(unsigned m, long long v) {
 #ifdef __CUDA_ARCH__
-  return __shfl_sync(m, v, 0, L);
-#else
-  return v;
+  if (G > 1) return __shfl_sync(m, v, 0, G);
 #endif
+  return v;
 }
 RLX_HD int ffs64(unsigned long long m) {
 #ifdef __CUDA_ARCH__
@@ -136,159 +158,230 @@ RLX_HD double defmem(int k) {
   return k == 0 ? 0.5 : k == 1 ? 0.55 : k == 2 ? 0.4 : k == 3 ? 0.3 : k == 4 ? 0.5 : k == 5 ? 0.6 : 0.05;
 }
 
-// Per-slice candidate scratch (shared memory).
-struct SliceCand {
-  double dur, mem, pre, suf, fin;
-  int kind, pipe, t, k, ins0, ins1, idle;
-  int twq_n, tw_run, pad;
-  uint16_t m[kMaxMembers];
-};
-
-struct Act {  // action started at pass begin
-  int cls;    // -1 none, 0 mux, 2 exclusive
-  int a, b, alloc;
-};
-
 RLX_HD unsigned long long dbits(double x) {
   unsigned long long b;
   memcpy(&b, &x, 8);
   return b == 0x8000000000000000ull ? 0ull : b;
 }
 
-RLX_HD bool key_less(unsigned long long a0, unsigned long long a1, unsigned long long a2,
-                                         unsigned long long b0, unsigned long long b1, unsigned long long b2) {
+RLX_HD bool key_less(unsigned long long a0, unsigned long long a1, unsigned long long a2, unsigned long long b0,
+                     unsigned long long b1, unsigned long long b2) {
   if (a0 != b0) return a0 < b0;
   if (a1 != b1) return a1 < b1;
   return a2 < b2;
 }
+// ---------------------------------------------------------------------------
+// Shared memory. The hot plan sits at offset 0 (staged by TMA), followed by
+// one slice per group. Addressing it through this symbol keeps every access
+// in the shared window (LDS/STS/ATOMS), not generic loads.
+extern __shared__ __align__(128) uint8_t rlx_smem[];
+#ifdef __CUDA_ARCH__
+#define SMEM rlx_smem
+#else
+extern uint8_t* g_twin_smem;
+#define SMEM g_twin_smem
+#endif
 
-template <int L, int WPL>
-struct Slice {
-  const double* lut;
+struct Act {  // action started at pass begin
+  int cls;    // -1 none, 0 multiplex, 2 exclusive
+  int a, b, alloc;
+};
+
+// Per-group candidate + pass-iterator state (shared memory).
+struct GroupCand {
+  double dur, mem, pre, suf;  // merged node M (merged_estimate :185-199, migration_cost :174-182)
+  double cost, fin;           // running candidate_cost and action_finish_estimate
+  double bytes;               // SURVEY §8(d) algorithmic bytes scored by this group
+  unsigned long long b0, b1, b2;  // best packed key of this group
+  unsigned long long passes, ncand, rm;
+  long long serial;
+  int kind, pipe, t, k, ins0, ins1, idle, cls;
+  int a, b, alloc, nwin;  // candidate action (non-merge)
+  int phase, y, oo, ai, mj, v;  // pass iterator
+  int fa, fb, falloc;     // follow-up action of the current pass
+  int twq_n, tw_run;
+  uint16_t m[kMaxMembers];
+};
+
+// Group slice layout (offsets in bytes from the slice start), stored in the
+// DevPlan constants by launch_score.
+RLX_HD void group_layout(DevPlan& P, int G, int WPL) {
+  uint32_t b = (uint32_t)((sizeof(GroupCand) + 15) & ~size_t(15));
+  P.g_mask = b;
+  b += 8u * P.W;
+  P.g_twend = b;
+  b += 8u * P.NTW;
+  P.g_grant = b;
+  b += P.has_penalty ? 8u * P.W * P.P : 0u;
+  P.g_pres = b;
+  b += 8u * G * WPL * 2;
+  P.g_ctr = b;
+  b += 4u * P.NC;
+  P.g_nds = b;
+  b += 4u * G * WPL * 2;
+  P.g_twq = b;
+  b += 2u * (P.NTW + 8);
+  P.g_bytes = (b + 15u) & ~15u;
+}
+
+template <int WPL>
+struct BitsFor {  // 2 bits per local worker
+  typedef typename std::conditional<(WPL > 16), unsigned long long, unsigned>::type type;
+};
+
+template <int G, int WPL>
+struct Lane {
+  typedef typename BitsFor<WPL>::type Bits;
+  static_assert(WPL <= 32, "at most 32 workers per lane");
+  const uint32_t gbase;  // slice offset in SMEM
   const int lane;
-  const unsigned smask;
-  // smem
-  unsigned* pend;
-  unsigned long long* mask;
-  double* twend;
-  uint16_t* twq;
-  double* grant;
-  SliceCand* sc;
-  int* gerr;
-  // per-worker registers
-  int nm[WPL];
-  int nd[WPL][2];
-  double rt[WPL][2], pr[WPL][2], wk[WPL][2];
-  bool pt[WPL][2];
-  // pass constants
+  const unsigned gm;
+  // registers: running members of this lane's workers (slot s of local worker j)
+  double wk[WPL][2], rt[WPL][2];
+  Bits rb;    // bit 2j+s: running
+  Bits pm;    // bit 2j+s: has a non-zero prefix (value in the slice)
+  Bits pf;    // bit 2j+s: still has a multiplex partner
+  double tl;  // this lane's next-event candidate time
+  int o, mt, ins, err;
+  // pass registers
+  double now, last;
+  int done_cnt, guard;
+  bool any_done;
+  // guard-failure report
   double* dbg = nullptr;
-  long long dbg_serial = -1;
-  int o;       // order index
-  int mt;      // merged target worker (-1: no merge)
-  int ins;     // insertion position on mt
-  int err;
+  int* dbg_flag = nullptr;
 
-  RLX_HD Slice(const double* l, int ln, unsigned m, uint8_t* base, int* ge)
-      : lut(l), lane(ln), smask(m), gerr(ge) {
-    uint8_t* q = base;
-    sc = reinterpret_cast<SliceCand*>(q);
-    q += (sizeof(SliceCand) + 15) & ~15;
-    mask = reinterpret_cast<unsigned long long*>(q);
-    q += sizeof(unsigned long long) * PLAN.W;
-    twend = reinterpret_cast<double*>(q);
-    q += sizeof(double) * PLAN.NTW;
-    grant = reinterpret_cast<double*>(q);
-    q += PLAN.has_penalty ? sizeof(double) * PLAN.W * PLAN.P : 0;
-    pend = reinterpret_cast<unsigned*>(q);
-    q += sizeof(unsigned) * PLAN.NT;
-    twq = reinterpret_cast<uint16_t*>(q);
+  RLX_HD Lane(uint32_t gb, int ln, unsigned m) : gbase(gb), lane(ln), gm(m) {
     err = 0;
+    rb = pm = pf = 0;
   }
 
-  // ---- node attributes (M = virtual merged node)
-  RLX_HD int kind(int n) const { return n == PLAN.M ? sc->kind : PLAN.kind[n]; }
-  RLX_HD int pipe(int n) const { return n == PLAN.M ? sc->pipe : PLAN.pipe[n]; }
-  RLX_HD double dur(int n) const { return n == PLAN.M ? sc->dur : PLAN.dur[n]; }
-  RLX_HD double memf(int n) const { return n == PLAN.M ? sc->mem : PLAN.mem[n]; }
-  RLX_HD double mpre(int n) const { return n == PLAN.M ? sc->pre : PLAN.mprefix[n]; }
-  RLX_HD int wrk(int n) const { return n == PLAN.M ? sc->t : PLAN.worker[n]; }
+  // ---- shared-memory views
+  RLX_HD GroupCand* gc() const { return reinterpret_cast<GroupCand*>(SMEM + gbase); }
+  RLX_HD unsigned long long* mask() const { return reinterpret_cast<unsigned long long*>(SMEM + gbase + PLAN.g_mask); }
+  RLX_HD double* twend() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_twend); }
+  RLX_HD double* grant() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_grant); }
+  RLX_HD double* pres() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_pres) + lane * WPL * 2; }
+  RLX_HD unsigned* ctr() const { return reinterpret_cast<unsigned*>(SMEM + gbase + PLAN.g_ctr); }
+  RLX_HD int* nds() const { return reinterpret_cast<int*>(SMEM + gbase + PLAN.g_nds) + lane * WPL * 2; }
+  RLX_HD uint16_t* twq() const { return reinterpret_cast<uint16_t*>(SMEM + gbase + PLAN.g_twq); }
+  template <class T>
+  RLX_HD const T* arr(uint32_t off) const {
+    return reinterpret_cast<const T*>(SMEM + off);
+  }
+  // ---- hot plan (shared memory)
+  RLX_HD int hkind(int n) const { return arr<uint8_t>(PLAN.o_kind)[n]; }
+  RLX_HD int hpipe(int n) const { return arr<uint8_t>(PLAN.o_pipe)[n]; }
+  RLX_HD int hworker(int n) const { return arr<uint16_t>(PLAN.o_worker)[n]; }
+  RLX_HD int hflags(int n) const { return arr<uint8_t>(PLAN.o_flags)[n]; }
+  RLX_HD double hdur(int n) const { return arr<double>(PLAN.o_dur)[n]; }
+  RLX_HD double hmem(int n) const { return arr<double>(PLAN.o_mem)[n]; }
+  RLX_HD double hmpre(int n) const { return arr<double>(PLAN.o_mprefix)[n]; }
+  RLX_HD double lutv(int i) const { return arr<double>(PLAN.o_lut)[i]; }
+  // node attributes (M = the candidate's virtual merged node)
+  RLX_HD int kind(int n) const { return n == PLAN.M ? gc()->kind : hkind(n); }
+  RLX_HD int pipe(int n) const { return n == PLAN.M ? gc()->pipe : hpipe(n); }
+  RLX_HD double dur(int n) const { return n == PLAN.M ? gc()->dur : hdur(n); }
+  RLX_HD double memf(int n) const { return n == PLAN.M ? gc()->mem : hmem(n); }
+  RLX_HD double mpre(int n) const { return n == PLAN.M ? gc()->pre : hmpre(n); }
+  RLX_HD int wrk(int n) const { return n == PLAN.M ? gc()->t : hworker(n); }
 
   RLX_HD double L3(int k, int partner, int alloc) {
-    double v = lut[(k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc];
+    double v = lutv((k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc);
     if (isnan(v)) err = RLX_ERR_KEY;
     return v;
   }
-
   RLX_HD int node_at(int w, int p) const {
     if (w == mt) {
       if (p == ins) return PLAN.M;
       if (p > ins) p--;
     }
-    return PLAN.ord[(o * PLAN.W + w) * kMaxPos + p];
+    return arr<uint16_t>(PLAN.o_ord)[(o * PLAN.W + w) * kMaxPos + p];
   }
   RLX_HD int pos_of(int n) const {
-    int p = PLAN.pos[o * PLAN.NL + n];
-    if (PLAN.worker[n] == mt && p >= ins) p++;
+    int p = arr<uint8_t>(PLAN.o_pos)[o * PLAN.NL + n];
+    if (hworker(n) == mt && p >= ins) p++;
     return p;
   }
 
-  // ---- completion bookkeeping
+  // ---- completion bookkeeping (succs of a completed node; readiness)
   RLX_HD void became_ready(int s) {
-    uint8_t f = PLAN.flags[s];
+    const int f = hflags(s);
     if (f & F_TW) {
-      int q = at_add(&sc->twq_n, 1);
-      twq[q] = (uint16_t)s;
+      const int q = at_add<G>(&gc()->twq_n, 1);
+      twq()[q] = (uint16_t)s;
+    } else if (f & F_WIN) {
+      at_or<G>(&mask()[hworker(s)], 1ull << pos_of(s));
+    }
+  }
+  RLX_HD void fire(int s) {
+    if (hflags(s) & F_JOIN) {  // a join releases its members, whose only predecessor it is
+      const int32_t* so = arr<int32_t>(PLAN.o_succ_off);
+      const uint16_t* sl = arr<uint16_t>(PLAN.o_succ);
+      for (int e = so[s], e1 = so[s + 1]; e < e1; e++) became_ready(sl[e]);
     } else {
-      at_or(&mask[PLAN.worker[s]], 1ull << pos_of(s));
+      became_ready(s);
     }
   }
   RLX_HD void dec(int s) {
-    unsigned old = at_sub(&pend[s], 1u);
-    if (old == 1u) {
-      if (PLAN.flags[s] & F_JOIN) {
-        for (int e = PLAN.succ_off[s]; e < PLAN.succ_off[s + 1]; e++) {
-          int s2 = PLAN.succ[e];
-          if (at_sub(&pend[s2], 1u) == 1u) became_ready(s2);
-        }
-      } else {
-        became_ready(s);
-      }
-    }
+    const unsigned c = arr<uint16_t>(PLAN.o_ctr_idx)[s];
+    if (c == 0xFFFFu || at_sub<G>(&ctr()[c], 1u) == 1u) fire(s);
   }
   RLX_HD void succs_of(int u) {
-    for (int e = PLAN.succ_off[u]; e < PLAN.succ_off[u + 1]; e++) dec(PLAN.succ[e]);
+    const int32_t* so = arr<int32_t>(PLAN.o_succ_off);
+    const uint16_t* sl = arr<uint16_t>(PLAN.o_succ);
+    for (int e = so[u], e1 = so[u + 1]; e < e1; e++) dec(sl[e]);
   }
   RLX_HD void complete(int n, unsigned& ld) {
     if (n == PLAN.M) {
       ld++;
-      for (int i = 0; i < sc->k; i++) succs_of(sc->m[i]);
+      const GroupCand* g = gc();
+      for (int i = 0; i < g->k; i++) succs_of(g->m[i]);
     } else {
-      if (PLAN.flags[n] & F_WIN) ld++;
+      if (hflags(n) & F_WIN) ld++;
       succs_of(n);
     }
   }
 
-  // ---- starting members (_start_member :460-484)
-  RLX_HD void start(int j, int w, int n, double rate, int alloc, bool partner) {
+  // ---- starting members (_start_member :460-484) on an idle local worker j
+  // (dynamic); slot s is compile-time.
+  RLX_HD void start(int j, int s, int w, int n, double rate, int alloc, bool partner) {
     double pre = mpre(n);
     if (PLAN.has_penalty && kind(n) <= RLX_KIND_DECODE_SMALL) {
-      double* g = &grant[w * PLAN.P + pipe(n)];
-      double am = PLAN.alloc_mem[alloc];
-      double last = *g;
-      if (!isnan(last) && fabs(last - am) > kEps) pre = pre + PLAN.realloc_penalty;
+      double* g = &grant()[w * PLAN.P + pipe(n)];
+      const double am = arr<double>(PLAN.o_alloc_mem)[alloc];
+      const double lastg = *g;
+      if (!isnan(lastg) && fabs(lastg - am) > kEps) pre = pre + PLAN.realloc_penalty;
       *g = am;
     }
-    double d = dur(n);
-    if (nm[j] == 0) {
-      nd[j][0] = n; rt[j][0] = rate; pr[j][0] = pre; wk[j][0] = d; pt[j][0] = partner;
+    const double d = dur(n);
+#pragma unroll
+    for (int jj = 0; jj < WPL; jj++)
+      if (jj == j) {
+        if (s == 0) {
+          wk[jj][0] = d;
+          rt[jj][0] = rate;
+        } else {
+          wk[jj][1] = d;
+          rt[jj][1] = rate;
+        }
+      }
+    const Bits bit = Bits(1) << (2 * j + s);
+    nds()[2 * j + s] = n;
+    rb |= bit;
+    if (partner) pf |= bit; else pf &= ~bit;
+    if (pre != 0.0) {
+      pm |= bit;
+      pres()[2 * j + s] = pre;
     } else {
-      nd[j][1] = n; rt[j][1] = rate; pr[j][1] = pre; wk[j][1] = d; pt[j][1] = partner;
+      pm &= ~bit;
     }
-    nm[j]++;
+    const double fe = (now + pre) + d * rate;
+    tl = fe < tl ? fe : tl;
   }
 
-  RLX_HD double rerated(double da, double sa, double db, double sb) const {
-    double na = da * sa, nb = db * sb;
+  RLX_HD static double rerated(double da, double sa, double db, double sb) {
+    const double na = da * sa, nb = db * sb;
     if (fabs(na - nb) <= kEps) return na;
     if (na < nb) return na + (1.0 - na / nb) * db;
     return nb + (1.0 - nb / na) * da;
@@ -296,14 +389,13 @@ struct Slice {
 
   // _best_pair_action :803-828
   RLX_HD bool best_pair(int a, int b, int& first, int& second, int& alloc) {
-    const double h = PLAN.headroom;
-    double ma = memf(a), mb = memf(b);
-    if (!(ma + mb <= 1.0 - h + 1e-12)) return false;
+    const double hr = PLAN.headroom;
+    const double ma = memf(a), mb = memf(b);
+    if (!(ma + mb <= 1.0 - hr + 1e-12)) return false;
     double best = INFINITY;
     bool found = false;
     const int ka = kind(a), kb = kind(b);
     const double da = dur(a), db = dur(b);
-#pragma unroll
     for (int oo = 0; oo < 2; oo++) {
       const int f = oo ? b : a, s = oo ? a : b;
       const int kf = oo ? kb : ka, ks = oo ? ka : kb;
@@ -311,9 +403,9 @@ struct Slice {
       const double ms = oo ? ma : mb;
       for (int ai = 0; ai < 3; ai++)
         for (int mj = 0; mj < 4; mj++) {
-          if (memgrid(mj) + ms > 1.0 - h + kEps) continue;
-          int al = 1 + ai * 4 + mj;
-          double e = rerated(df, L3(kf, ks, al), ds, L3(ks, kf, al + 12));
+          if (memgrid(mj) + ms > 1.0 - hr + kEps) continue;
+          const int al = 1 + ai * 4 + mj;
+          const double e = rerated(df, L3(kf, ks, al), ds, L3(ks, kf, al + 12));
           if (e < best - kEps) {
             best = e;
             first = f;
@@ -326,504 +418,630 @@ struct Slice {
     return found;
   }
 
-  // One pass of _complete_window with action `act` applied first.
-  RLX_HD double pass(int variant, const Act& act, bool is_merge, int nwin, unsigned long long& passes,
-                         double& bytes) {
+  // ---- pass initialisation: decision state + `act` applied (window_cost :886-887)
+  RLX_HD void init_pass(int variant, const Act& act, bool is_merge) {
+    GroupCand* g = gc();
     o = variant == 2 ? 1 : 0;
-    const bool pair = variant == 1;
-    mt = is_merge ? sc->t : -1;
-    ins = is_merge ? (o ? sc->ins1 : sc->ins0) : -1;
-    for (int i = lane; i < PLAN.NT; i += L) pend[i] = PLAN.pend0[i];
-    for (int w = lane; w < PLAN.W; w += L) mask[w] = PLAN.mask0[o * PLAN.W + w];
-    for (int i = lane; i < PLAN.NTW; i += L) twend[i] = PLAN.tw_end0[i];
+    mt = is_merge ? g->t : -1;
+    ins = is_merge ? (o ? g->ins1 : g->ins0) : -1;
+    now = PLAN.now;
+    last = 0.0;
+    done_cnt = 0;
+    guard = 0;
+    any_done = false;
+    const int W = PLAN.W;
+    unsigned long long* mk = mask();
+    unsigned* ct = ctr();
+    double* te = twend();
+    for (int i = lane; i < PLAN.NC; i += G) ct[i] = PLAN.ctr0[i];
+    for (int w = lane; w < W; w += G) mk[w] = PLAN.mask0[o * W + w];
+    for (int i = lane; i < PLAN.NTW; i += G) te[i] = PLAN.tw_end0[i];
     if (PLAN.has_penalty)
-      for (int i = lane; i < PLAN.W * PLAN.P; i += L) grant[i] = PLAN.grant0[i];
+      for (int i = lane; i < W * PLAN.P; i += G) grant()[i] = PLAN.grant0[i];
+    gsync<G>(gm);
     if (lane == 0) {
-      sc->twq_n = 0;
-      sc->tw_run = PLAN.n_tw_run0;
+      g->twq_n = 0;
+      g->tw_run = PLAN.n_tw_run0;
     }
+    rb = pm = pf = 0;
+    tl = INFINITY;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
-      int w = lane + L * j;
-      nm[j] = 0;
-      if (w < PLAN.W) {
-        int c = PLAN.nmem0[w];
+      const int w = lane + G * j;
+      if (w < W) {
+        const int c = PLAN.nmem0[w];
+#pragma unroll
         for (int s = 0; s < 2; s++)
           if (s < c) {
-            nd[j][s] = PLAN.mnode0[2 * w + s];
-            rt[j][s] = PLAN.mrate0[2 * w + s];
-            pr[j][s] = PLAN.mpre0[2 * w + s];
-            wk[j][s] = PLAN.mwork0[2 * w + s];
-            pt[j][s] = PLAN.mpart0[2 * w + s] != 0;
+            const Bits bit = Bits(1) << (2 * j + s);
+            const double r = PLAN.mrate0[2 * w + s], p = PLAN.mpre0[2 * w + s], wv = PLAN.mwork0[2 * w + s];
+            nds()[2 * j + s] = PLAN.mnode0[2 * w + s];
+            rt[j][s] = r;
+            wk[j][s] = wv;
+            rb |= bit;
+            if (PLAN.mpart0[2 * w + s]) pf |= bit;
+            if (p != 0.0) {
+              pm |= bit;
+              pres()[2 * j + s] = p;
+            }
+            const double fe = (now + p) + wv * r;
+            tl = fe < tl ? fe : tl;
           }
-        nm[j] = c;
       }
     }
-    wsync(smask);
-    if (is_merge && lane == 0) {
-      unsigned long long m = mask[mt];
-      unsigned long long lo = ins ? (m & ((1ull << ins) - 1)) : 0ull;
-      mask[mt] = lo | ((m >> ins) << (ins + 1)) | (1ull << ins);
-      for (int i = 0; i < sc->k; i++) {
-        int x = sc->m[i];
-        mask[PLAN.worker[x]] &= ~(1ull << pos_of(x));
+    if (PLAN.n_tw_run0)  // tool waits running at the decision state
+      for (int i = lane; i < PLAN.NTW; i += G) tl = te[i] < tl ? te[i] : tl;
+    if (is_merge && lane == 0) {  // the merged node replaces its members in the ready masks
+      const unsigned long long m = mk[mt];
+      const unsigned long long lo = ins ? (m & ((1ull << ins) - 1)) : 0ull;
+      mk[mt] = lo | ((m >> ins) << (ins + 1)) | (1ull << ins);
+      for (int i = 0; i < g->k; i++) {
+        const int x = g->m[i];
+        mk[hworker(x)] &= ~(1ull << pos_of(x));
       }
     }
-    wsync(smask);
-    int R0 = PLAN.n_run0;
+    gsync<G>(gm);
     if (act.cls >= 0) {
-      int w = wrk(act.a);
-      R0 += act.cls == 0 ? 2 : 1;
-      if ((w % L) == lane) {
-        int j = w / L;
-#pragma unroll
-        for (int jj = 0; jj < WPL; jj++)
-          if (jj == j) {
-            if (act.cls == 2) {
-              mask[w] &= ~(1ull << (act.a == PLAN.M ? ins : pos_of(act.a)));
-              start(jj, w, act.a, L3(kind(act.a), -1, 0), 0, false);
-            } else {
-              int a = act.a, b = act.b;
-              mask[w] &= ~((1ull << (a == PLAN.M ? ins : pos_of(a))) | (1ull << (b == PLAN.M ? ins : pos_of(b))));
-              double ra = L3(kind(a), kind(b), act.alloc);
-              double rb = L3(kind(b), kind(a), act.alloc + 12);
-              start(jj, w, a, ra, act.alloc, true);
-              start(jj, w, b, rb, act.alloc + 12, true);
-            }
-          }
-      }
-    }
-    wsync(smask);
-    // algorithmic bytes of this pass
-    passes++;
-    bytes += 32.0 * nwin + 4.0 * (double)PLAN.ew + 32.0 * R0 + 16.0 * PLAN.n_tw_run0;
-
-    double now = PLAN.now;
-    double last = 0.0;
-    bool any_done = false;
-    int done_cnt = 0;
-    int guard = 0;
-    for (;;) {
-      if (done_cnt >= nwin) break;
-      // ---- selection on idle workers (one sweep)
-#pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        int w = lane + L * j;
-        if (w < PLAN.W && nm[j] == 0) {
-          unsigned long long m = mask[w];
-          if (m) {
-            int p = ffs64(m) - 1;
-            int x = node_at(w, p);
-            int first = x, second = -1, al = 0;
-            bool paired = false;
-            if (pair) {
-              unsigned long long m2 = m & (m - 1);
-              int px = pipe(x);
-              while (m2) {
-                int q = ffs64(m2) - 1;
-                int y = node_at(w, q);
-                if (pipe(y) != px) {
-                  paired = best_pair(x, y, first, second, al);
-                  if (paired) m &= ~(1ull << q);
-                  break;
-                }
-                m2 &= m2 - 1;
-              }
-            }
-            m &= ~(1ull << p);
-            mask[w] = m;
-            if (paired) {
-              double ra = L3(kind(first), kind(second), al);
-              double rb = L3(kind(second), kind(first), al + 12);
-              start(j, w, first, ra, al, true);
-              start(j, w, second, rb, al + 12, true);
-            } else {
-              start(j, w, x, L3(kind(x), -1, 0), 0, false);
-            }
-          }
+      const int w = wrk(act.a);
+      if ((w % G) == lane) {
+        const int j = w / G;
+        if (act.cls == 2) {
+          mk[w] &= ~(1ull << (act.a == PLAN.M ? ins : pos_of(act.a)));
+          start(j, 0, w, act.a, L3(kind(act.a), -1, 0), 0, false);
+        } else {
+          const int a = act.a, b = act.b;
+          mk[w] &= ~((1ull << (a == PLAN.M ? ins : pos_of(a))) | (1ull << (b == PLAN.M ? ins : pos_of(b))));
+          const double ra = L3(kind(a), kind(b), act.alloc);
+          const double rbv = L3(kind(b), kind(a), act.alloc + 12);
+          start(j, 0, w, a, ra, act.alloc, true);
+          start(j, 1, w, b, rbv, act.alloc + 12, true);
         }
       }
-      // ---- has_events
-      bool mine = false;
+    }
+    gsync<G>(gm);
+  }
+
+  // ---- selection on idle workers (one sweep)
+  RLX_HD void select(bool pair) {
+    const int W = PLAN.W;
+    unsigned idle = 0;
 #pragma unroll
-      for (int j = 0; j < WPL; j++) mine |= nm[j] > 0;
-      wsync(smask);
-      const int twr = sc->tw_run;
-      if (!wany(smask, mine) && twr == 0) break;
-      // ---- next event time
-      double t = INFINITY;
-#pragma unroll
-      for (int j = 0; j < WPL; j++)
-        for (int s = 0; s < 2; s++)
-          if (s < nm[j]) {
-            double fe = (now + pr[j][s]) + wk[j][s] * rt[j][s];
-            t = fe < t ? fe : t;
+    for (int j = 0; j < WPL; j++)
+      if (lane + G * j < W && !((rb >> (2 * j)) & Bits(3))) idle |= 1u << j;
+    unsigned long long* mk = mask();
+    while (idle) {
+      const int j = ffs64(idle) - 1;
+      idle &= idle - 1;
+      const int w = lane + G * j;
+      unsigned long long m = mk[w];
+      if (!m) continue;
+      const int p = ffs64(m) - 1;
+      const int x = node_at(w, p);
+      int first = x, second = -1, al = 0;
+      bool paired = false;
+      if (pair) {
+        unsigned long long m2 = m & (m - 1);
+        const int px = pipe(x);
+        while (m2) {
+          const int q = ffs64(m2) - 1;
+          const int y = node_at(w, q);
+          if (pipe(y) != px) {
+            paired = best_pair(x, y, first, second, al);
+            if (paired) m &= ~(1ull << q);
+            break;
           }
-      if (twr)
-        for (int i = lane; i < PLAN.NTW; i += L) t = twend[i] < t ? twend[i] : t;
-      t = wmin<L>(smask, t);
-      double dt = t - now;
-      if (!(dt > 0.0)) dt = 0.0;
-      now = t;
-      // ---- consume + finished members
-      unsigned ld = 0;
-      bool fin_any = false;
+          m2 &= m2 - 1;
+        }
+      }
+      m &= ~(1ull << p);
+      mk[w] = m;
+      if (paired) {
+        const double ra = L3(kind(first), kind(second), al);
+        const double rbv = L3(kind(second), kind(first), al + 12);
+        start(j, 0, w, first, ra, al, true);
+        start(j, 1, w, second, rbv, al + 12, true);
+      } else {
+        start(j, 0, w, x, L3(kind(x), -1, 0), 0, false);
+      }
+    }
+  }
+
+  // ---- advance (:593-627): consume dt on this lane's members, re-rate the
+  // survivors of finished pairs, fold every survivor's next finish estimate
+  // into tl, then complete the finished nodes.
+  RLX_HD void consume(double dt, unsigned& ld) {
+    tl = INFINITY;
+    Bits fb = 0;
+    double* pr = pres();
 #pragma unroll
-      for (int j = 0; j < WPL; j++) {
-        bool f0 = false, f1 = false;
-        for (int s = 0; s < 2; s++)
-          if (s < nm[j]) {
-            double d = dt;
-            double p = pr[j][s];
+    for (int j = 0; j < WPL; j++) {
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        const Bits bit = Bits(1) << (2 * j + s);
+        if (rb & bit) {
+          double d = dt;
+          double p = 0.0;
+          if (pm & bit) {
+            p = pr[2 * j + s];
             if (p > kEps) {
-              double used = d < p ? d : p;
+              const double used = d < p ? d : p;
               p = p - used;
               d = d - used;
-              pr[j][s] = p;
-            }
-            double wv = wk[j][s];
-            double r = rt[j][s];
-            if (d > kEps && wv > kEps) {
-              double q = (r == 1.0) ? d : d / r;
-              double z = wv - q;
-              wv = z > 0.0 ? z : 0.0;
-              wk[j][s] = wv;
-            }
-            bool f = p <= kEps && wv * r <= kEps;
-            if (s == 0) f0 = f; else f1 = f;
-          }
-        if (f0 || f1) {
-          fin_any = true;
-          if (f0) complete(nd[j][0], ld);
-          if (nm[j] == 2 && f1) complete(nd[j][1], ld);
-          if (nm[j] == 2 && f0 != f1) {
-            // survivor re-rated to its exclusive speed (:615-621)
-            int s = f0 ? 1 : 0;
-            double r = rt[j][s];
-            bool pp = pt[j][s];
-            if (pp) r = 1.0;
-            nd[j][0] = nd[j][s];
-            rt[j][0] = r;
-            pr[j][0] = pr[j][s];
-            wk[j][0] = wk[j][s];
-            pt[j][0] = false;
-            nm[j] = 1;
-          } else {
-            nm[j] = 0;
-          }
-        }
-      }
-      wsync(smask);
-      // ---- tool-wait expiry
-      bool exp_any = false;
-      if (twr) {
-        int ex = 0;
-        for (int i = lane; i < PLAN.NTW; i += L)
-          if (twend[i] <= now + kEps) {
-            twend[i] = INFINITY;
-            complete(PLAN.tw_node[i], ld);
-            ex++;
-          }
-        if (ex) {
-          at_add(&sc->tw_run, -ex);
-          exp_any = true;
-        }
-      }
-      wsync(smask);
-      // ---- auto-start ready tool waits (:421-434)
-      if (wany(smask, fin_any || exp_any)) {
-        if (lane == 0) {
-          while (sc->twq_n > 0) {
-            int s = twq[--sc->twq_n];
-            double dd = PLAN.dur[s];
-            if (dd <= kEps) {
-              complete(s, ld);
-            } else {
-              twend[PLAN.tw_slot[s]] = now + dd;
-              sc->tw_run++;
+              pr[2 * j + s] = p;
             }
           }
+          double wv = wk[j][s];
+          const double r = rt[j][s];
+          if (d > kEps && wv > kEps) {
+            const double q = (r == 1.0) ? d : d / r;
+            const double z = wv - q;
+            wv = z > 0.0 ? z : 0.0;
+            wk[j][s] = wv;
+          }
+          if (p <= kEps && wv * r <= kEps) fb |= bit;
         }
-        wsync(smask);
       }
-      unsigned tot = wsum(smask, ld);
-      if (tot) {
-        done_cnt += (int)tot;
-        last = now;
-        any_done = true;
-      }
-      if (++guard > 10000) {
-        err = RLX_ERR_SCHEDULING;
-        if (lane == 0 && dbg && dbg[0] == 0.0 && (dbg[0] = 1.0) == 1.0) {
-          int live = 0;
-          for (int i = 0; i < PLAN.NTW; i++) live += twend[i] != INFINITY;
-          dbg[1] = (double)dbg_serial;
-          dbg[2] = variant;
-          dbg[3] = now;
-          dbg[4] = done_cnt;
-          dbg[5] = nwin;
-          dbg[6] = twr;
-          dbg[7] = live;
-          dbg[8] = sc->twq_n;
-          dbg[9] = nm[0];
-          dbg[10] = act.cls;
-          dbg[11] = act.a;
-          dbg[12] = mt;
+      const Bits both = Bits(3) << (2 * j);
+      if (fb & both) {
+        // a survivor whose partner finished drops to its exclusive speed (:615-621)
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if ((rb & bit) && !(fb & bit) && (pf & bit)) {
+            rt[j][s] = 1.0;
+            pf &= ~bit;
+          }
         }
-        break;
+        rb &= ~(fb & both);
+      }
+#pragma unroll
+      for (int s = 0; s < 2; s++) {  // finish_estimate :328
+        const Bits bit = Bits(1) << (2 * j + s);
+        if (rb & bit) {
+          const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
+          const double fe = (now + p) + wk[j][s] * rt[j][s];
+          tl = fe < tl ? fe : tl;
+        }
       }
     }
-    return any_done ? last : now;
+    const int* nd = nds();
+    while (fb) {
+      const int i = ffs64(fb) - 1;
+      fb &= fb - 1;
+      complete(nd[i], ld);
+    }
+  }
+
+  // ---- one simulated event of _complete_window (:833-867). Returns true
+  // while the pass continues; on false `now`/`last`/`any_done` hold the result.
+  RLX_HD bool step(bool pair, int nwin, long long serial, int variant) {
+    select(pair);
+    const bool mine = rb != Bits(0);
+    gsync<G>(gm);
+    GroupCand* g = gc();
+    const int twr = g->tw_run;
+    if (!gany<G>(gm, mine) && twr == 0) return false;  // has_events
+    const double t = gmin<G>(gm, tl);
+    if (++guard > 10000) {  // scheduler.py:866-867
+      err = RLX_ERR_SCHEDULING;
+      if (dbg && lane == 0 && at_cas(dbg_flag, 0, 1) == 0) {
+        dbg[1] = (double)serial;
+        dbg[2] = variant;
+        dbg[3] = now;
+        dbg[4] = done_cnt;
+        dbg[5] = nwin;
+        dbg[6] = twr;
+        dbg[12] = mt;
+      }
+      return false;
+    }
+    double dt = t - now;
+    if (!(dt > 0.0)) dt = 0.0;
+    now = t;
+    unsigned ld = 0;
+    consume(dt, ld);
+    gsync<G>(gm);
+    // tool waits: expiry (:622-626) and auto-start of ready ones (:421-434)
+    if (twr) {
+      int ex = 0;
+      double* te = twend();
+      for (int i = lane; i < PLAN.NTW; i += G) {
+        const double e = te[i];
+        if (e <= now + kEps) {
+          te[i] = INFINITY;
+          complete(arr<uint16_t>(PLAN.o_tw_node)[i], ld);
+          ex++;
+        } else {
+          tl = e < tl ? e : tl;
+        }
+      }
+      if (ex) at_add<G>(&g->tw_run, -ex);
+      gsync<G>(gm);
+    }
+    if (g->twq_n > 0) {
+      gsync<G>(gm);
+      if (lane == 0) {
+        uint16_t* q = twq();
+        double* te = twend();
+        while (g->twq_n > 0) {
+          const int s = q[--g->twq_n];
+          const double dd = hdur(s);
+          if (dd <= kEps) {
+            complete(s, ld);
+          } else {
+            const double e = now + dd;
+            te[arr<int16_t>(PLAN.o_tw_slot)[s]] = e;
+            g->tw_run++;
+            tl = e < tl ? e : tl;
+          }
+        }
+      }
+      gsync<G>(gm);
+    }
+    const unsigned tot = gsum<G>(gm, ld);
+    if (tot) {
+      done_cnt += (int)tot;
+      last = now;
+      any_done = true;
+    }
+    return done_cnt < nwin;
   }
 };
 
-// The candidate loop of one slice (device: one warp fraction; host twin: one lane).
-template <int L, int WPL>
-RLX_HD void slice_loop(const WorkDesc& wd, const double* lut, uint8_t* base, int lane, unsigned smask,
-                       SliceOut* out) {
-  Slice<L, WPL> S(lut, lane, smask, base, wd.err);
-  S.dbg = wd.dbg;
-  SliceCand* sc = S.sc;
-
-  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull;
-  unsigned long long passes = 0, ncand = 0;
-  double bytes = 0.0;
-  const int64_t total = wd.na + wd.nb + wd.nc;
-  for (;;) {
-    long long g = 0;
-    if (lane == 0) {
-      g = (long long)at_add64(wd.counter, 1ull);
-      if (*(volatile int*)wd.err) g = total;
-    }
-    g = wbcast<L>(smask, g);
-    if (g >= total) break;
-    int64_t serial = g < wd.na ? wd.a0 + g : (g < wd.na + wd.nb ? wd.b0 + (g - wd.na) : wd.c0 + (g - wd.na - wd.nb));
-    Cand c;
-    decode_serial(PLAN, serial, c);
-    S.dbg_serial = serial;
-    double cost = INFINITY, fin;
-    if (c.cls == 1) {
-      // ---- merged node (_apply_merge :517-581, merged_estimate :185-199)
-      if (lane == 0) {
-        long long tokens = 0, active = 0;
-        double dmax = 0.0, mmax = 0.0, sfx = 0.0;
-        int p = PLAN.pipe[c.m[0]];
-        for (int i = 0; i < c.k; i++) {
-          int x = c.m[i];
-          sc->m[i] = (uint16_t)x;
-          tokens += PLAN.rem[x];
-          active += PLAN.act[x];
-          if (i == 0 || PLAN.dur[x] > dmax) dmax = PLAN.dur[x];
-          if (i == 0 || PLAN.mem[x] > mmax) mmax = PLAN.mem[x];
-          if (i == 0 || PLAN.msx[x] > sfx) sfx = PLAN.msx[x];
-        }
-        int kd;
-        double du;
-        if (active <= 0) {
-          kd = PLAN.kind[c.m[0]];
-          du = dmax;
+// Merged node of a Merge candidate (_apply_merge :517-581, merged_estimate
+// :185-199, migration_cost :174-182) and its insertion point in both worker
+// orders (ids compare as Python str). Group leader only.
+RLX_HD void setup_merge(const Cand& c, GroupCand* sc, int* gerr) {
+  long long tokens = 0, active = 0;
+  double dmax = 0.0, mmax = 0.0, sfx = 0.0;
+  const int p = PLAN.pipe[c.m[0]];
+  for (int i = 0; i < c.k; i++) {
+    const int x = c.m[i];
+    sc->m[i] = (uint16_t)x;
+    tokens += PLAN.rem[x];
+    active += PLAN.act[x];
+    if (i == 0 || PLAN.dur[x] > dmax) dmax = PLAN.dur[x];
+    if (i == 0 || PLAN.mem[x] > mmax) mmax = PLAN.mem[x];
+    if (i == 0 || PLAN.msx[x] > sfx) sfx = PLAN.msx[x];
+  }
+  int kd;
+  double du;
+  if (active <= 0) {
+    kd = PLAN.kind[c.m[0]];
+    du = dmax;
+  } else {
+    const int bk = active >= 1024 ? 2 : (active >= 128 ? 1 : 0);
+    kd = bk == 0 ? RLX_KIND_DECODE_SMALL : (bk == 1 ? RLX_KIND_DECODE_MEDIUM : RLX_KIND_DECODE_LARGE);
+    if (!PLAN.latency_ok[p * 3 + bk]) at_cas(gerr, 0, RLX_ERR_KEY);
+    du = ((double)tokens * PLAN.latency[p * 3 + bk]) / (double)active;
+  }
+  double pre = 0.0;
+  for (int i = 0; i < c.k; i++)
+    if (PLAN.worker[c.m[i]] != c.target) pre = pre + PLAN.migc[c.m[i]];
+  const double dm = defmem(kd);
+  sc->kind = kd;
+  sc->dur = du;
+  sc->mem = mmax > dm ? mmax : dm;
+  sc->pre = pre;
+  sc->suf = du + sfx;
+  sc->pipe = p;
+  sc->t = c.target;
+  sc->k = c.k;
+  sc->idle = PLAN.nmem0[c.target] == 0;
+  const int t = c.target;
+  const int cnt = PLAN.ord_cnt[t];
+  const int prk = PLAN.pipe_rank[p];
+  for (int oo = 0; oo < 2; oo++) {
+    int ins = cnt;
+    for (int q = 0; q < cnt; q++) {
+      const int y = PLAN.ord[(oo * PLAN.W + t) * kMaxPos + q];
+      bool y_first;
+      if (oo == 0 && PLAN.suffix[y] != sc->suf) {
+        y_first = PLAN.suffix[y] > sc->suf;
+      } else {
+        const int yr = PLAN.pipe_rank[PLAN.pipe[y]];
+        if (yr != prk) {
+          y_first = yr < prk;
+        } else if (PLAN.lt_merge[y] != 2) {
+          y_first = PLAN.lt_merge[y] == 1;
         } else {
-          int bk = active >= 1024 ? 2 : (active >= 128 ? 1 : 0);
-          kd = bk == 0 ? RLX_KIND_DECODE_SMALL : (bk == 1 ? RLX_KIND_DECODE_MEDIUM : RLX_KIND_DECODE_LARGE);
-          if (!PLAN.latency_ok[p * 3 + bk]) at_cas(wd.err, 0, RLX_ERR_KEY);
-          du = ((double)tokens * PLAN.latency[p * 3 + bk]) / (double)active;
-        }
-        double pre = 0.0;
-        for (int i = 0; i < c.k; i++)
-          if (PLAN.worker[c.m[i]] != c.target) pre = pre + PLAN.migc[c.m[i]];
-        double dm = defmem(kd);
-        sc->kind = kd;
-        sc->dur = du;
-        sc->mem = mmax > dm ? mmax : dm;
-        sc->pre = pre;
-        sc->suf = du + sfx;
-        sc->pipe = p;
-        sc->t = c.target;
-        sc->k = c.k;
-        sc->idle = PLAN.nmem0[c.target] == 0;
-        // insertion position of the merged node in each worker order
-        const int t = c.target;
-        const int cnt = PLAN.ord_cnt[t];
-        const int prk = PLAN.pipe_rank[p];
-        for (int oo = 0; oo < 2; oo++) {
-          int ins = cnt;
-          for (int q = 0; q < cnt; q++) {
-            int y = PLAN.ord[(oo * PLAN.W + t) * kMaxPos + q];
-            bool y_first;
-            if (oo == 0 && PLAN.suffix[y] != sc->suf) {
-              y_first = PLAN.suffix[y] > sc->suf;
-            } else {
-              int yr = PLAN.pipe_rank[PLAN.pipe[y]];
-              if (yr != prk) {
-                y_first = yr < prk;
-              } else if (PLAN.lt_merge[y] != 2) {
-                y_first = PLAN.lt_merge[y] == 1;
+          // id(y) vs "merge[" + "+".join(member ids) + "]@w<t>"
+          const char* ys = PLAN.ids + PLAN.id_off[y];
+          int seg = -1;
+          const char* cp = "merge[";
+          char tail[16];
+          const int wid = PLAN.worker_ids[t];
+          int tl = 0;
+          tail[tl++] = ']';
+          tail[tl++] = '@';
+          tail[tl++] = 'w';
+          {
+            char tmp[12];
+            int nt = 0;
+            unsigned v = wid < 0 ? (unsigned)(-wid) : (unsigned)wid;
+            do {
+              tmp[nt++] = (char)('0' + v % 10);
+              v /= 10;
+            } while (v);
+            if (wid < 0) tail[tl++] = '-';
+            while (nt) tail[tl++] = tmp[--nt];
+          }
+          tail[tl] = 0;
+          int cmp = 0;
+          for (;;) {
+            while (*cp == 0) {
+              seg++;
+              if (seg < 2 * c.k - 1) {
+                cp = (seg & 1) ? "+" : PLAN.ids + PLAN.id_off[c.m[seg >> 1]];
+              } else if (seg == 2 * c.k - 1) {
+                cp = tail;
               } else {
-                // id(y) vs "merge[" + "+".join(member ids) + "]@w<t>"
-                const char* ys = PLAN.ids + PLAN.id_off[y];
-                int seg = -1;
-                const char* cp = "merge[";
-                char tail[16];
-                int wid = PLAN.worker_ids[t];
-                int tl = 0;
-                tail[tl++] = ']';
-                tail[tl++] = '@';
-                tail[tl++] = 'w';
-                {
-                  char tmp[12];
-                  int nt = 0;
-                  unsigned v = wid < 0 ? (unsigned)(-wid) : (unsigned)wid;
-                  do { tmp[nt++] = (char)('0' + v % 10); v /= 10; } while (v);
-                  if (wid < 0) tail[tl++] = '-';
-                  while (nt) tail[tl++] = tmp[--nt];
-                }
-                tail[tl] = 0;
-                int cmp = 0;
-                for (;;) {
-                  char mc;
-                  while (*cp == 0) {
-                    seg++;
-                    if (seg < 2 * c.k - 1) {
-                      cp = (seg & 1) ? "+" : PLAN.ids + PLAN.id_off[c.m[seg >> 1]];
-                    } else if (seg == 2 * c.k - 1) {
-                      cp = tail;
-                    } else {
-                      break;
-                    }
-                  }
-                  mc = *cp;
-                  unsigned char yc = (unsigned char)*ys;
-                  unsigned char vc = (unsigned char)mc;
-                  if (yc != vc) {
-                    cmp = yc < vc ? -1 : 1;
-                    break;
-                  }
-                  if (yc == 0) break;
-                  ys++;
-                  cp++;
-                }
-                y_first = cmp < 0;
+                break;
               }
             }
-            if (!y_first) {
-              ins = q;
+            const unsigned char yc = (unsigned char)*ys;
+            const unsigned char vc = (unsigned char)*cp;
+            if (yc != vc) {
+              cmp = yc < vc ? -1 : 1;
               break;
             }
+            if (yc == 0) break;
+            ys++;
+            cp++;
           }
-          if (oo == 0) sc->ins0 = ins; else sc->ins1 = ins;
+          y_first = cmp < 0;
         }
       }
-      wsync(smask);
-      fin = (PLAN.now + sc->pre) + sc->dur;
-      const int nwin = PLAN.NWIN - c.k + 1;
-      if (sc->idle) {
-        // follow-ups on the merged node (candidate_cost :907-918)
-        Act a{2, PLAN.M, -1, 0};
-        for (int v = 0; v < 3; v++) {
-          double x = S.pass(v, a, true, nwin, passes, bytes);
-          cost = x < cost ? x : cost;
-        }
-        const int t = sc->t;
-        unsigned long long rm = PLAN.mask0[1 * PLAN.W + t];
-        const double h = PLAN.headroom;
-        while (rm) {
-          int q = ffs64(rm) - 1;
-          rm &= rm - 1;
-          int y = PLAN.ord[(1 * PLAN.W + t) * kMaxPos + q];
-          bool member = false;
-          for (int i = 0; i < sc->k; i++) member |= sc->m[i] == y;
-          if (member || PLAN.pipe[y] == sc->pipe) continue;
-          if (!(sc->mem + PLAN.mem[y] <= 1.0 - h + 1e-12)) continue;
-          for (int oo = 0; oo < 2; oo++) {
-            int f = oo ? y : PLAN.M, s = oo ? PLAN.M : y;
-            double ms = oo ? sc->mem : PLAN.mem[y];
-            for (int ai = 0; ai < 3; ai++)
-              for (int mj = 0; mj < 4; mj++) {
-                if (memgrid(mj) + ms > 1.0 - h + kEps) continue;
-                Act m{0, f, s, 1 + ai * 4 + mj};
-                for (int v = 0; v < 3; v++) {
-                  double x = S.pass(v, m, true, nwin, passes, bytes);
-                  cost = x < cost ? x : cost;
-                }
-              }
-          }
-        }
-      } else {
-        Act a{-1, -1, -1, 0};
-        for (int v = 0; v < 3; v++) {
-          double x = S.pass(v, a, true, nwin, passes, bytes);
-          cost = x < cost ? x : cost;
-        }
+      if (!y_first) {
+        ins = q;
+        break;
       }
+    }
+    if (oo == 0) sc->ins0 = ins; else sc->ins1 = ins;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pass iterator of one candidate (candidate_cost :902-918 / window_cost
+// :878-899): variants innermost; a merge onto an idle target runs Exclusive(M)
+// and then every Multiplex follow-up touching M (orientation x alpha x mem,
+// feasible only), a merge onto a busy target runs the merge alone.
+// Returns false when the candidate has no further pass. Group-uniform.
+RLX_HD bool next_action(GroupCand* g) {
+  if (g->v < 2) {
+    g->v++;
+    // variant 2 (name order) repeats variant 0 (suffix order) exactly when
+    // both orders coincide on every worker, the merged node included
+    if (!(g->v == 2 && PLAN.same_order && (g->cls != 1 || g->ins0 == g->ins1))) return true;
+  }
+  g->v = 0;
+  if (g->cls != 1 || !g->idle) return false;
+  const double hr = PLAN.headroom;
+  // advance (y, oo, ai, mj) to the next feasible follow-up
+  for (;;) {
+    if (g->phase == 0) {
+      g->phase = 1;
+      g->y = -1;
     } else {
-      S.mt = -1;
-      S.ins = -1;
-      Act a{c.cls, c.a, c.cls == 0 ? c.b : -1, c.alloc};
-      // action_finish_estimate :773-789 (with the realloc penalty of the decision state)
-      auto fin_of = [&](int n, int alloc) {
-        double pre = PLAN.mprefix[n];
-        if (PLAN.has_penalty && PLAN.kind[n] <= RLX_KIND_DECODE_SMALL) {
-          double g = PLAN.grant0[PLAN.worker[n] * PLAN.P + PLAN.pipe[n]];
-          if (!isnan(g) && fabs(g - PLAN.alloc_mem[alloc]) > kEps) pre = pre + PLAN.realloc_penalty;
-        }
-        return pre;
-      };
-      if (c.cls == 2) {
-        double r = S.L3(PLAN.kind[c.a], -1, 0);
-        fin = (PLAN.now + fin_of(c.a, 0)) + PLAN.dur[c.a] * r;
-      } else {
-        double ra = S.L3(PLAN.kind[c.a], PLAN.kind[c.b], c.alloc);
-        double rb = S.L3(PLAN.kind[c.b], PLAN.kind[c.a], c.alloc + 12);
-        double fa = (PLAN.now + fin_of(c.a, c.alloc)) + PLAN.dur[c.a] * ra;
-        double fb = (PLAN.now + fin_of(c.b, c.alloc + 12)) + PLAN.dur[c.b] * rb;
-        fin = fb > fa ? fb : fa;
-      }
-      for (int v = 0; v < 3; v++) {
-        double x = S.pass(v, a, false, PLAN.NWIN, passes, bytes);
-        cost = x < cost ? x : cost;
-      }
+      if (++g->mj < 4) goto check;
+      g->mj = 0;
+      if (++g->ai < 3) goto check;
+      g->ai = 0;
+      if (++g->oo < 2) goto check;
+      g->y = -1;
     }
-    if (S.err) at_cas(wd.err, 0, S.err);
-    ncand++;
-    unsigned long long k0 = dbits(cost), k1 = dbits(fin);
-    unsigned long long k2 = ((unsigned long long)c.cls << 61) | (unsigned long long)serial;
-    if (key_less(k0, k1, k2, b0, b1, b2)) {
-      b0 = k0;
-      b1 = k1;
-      b2 = k2;
+    // next partner on the target worker (ready at the decision, name order)
+    for (;;) {
+      if (!g->rm) return false;
+      const int q = ffs64(g->rm) - 1;
+      g->rm &= g->rm - 1;
+      const int y = PLAN.ord[(1 * PLAN.W + g->t) * kMaxPos + q];
+      bool member = false;
+      for (int i = 0; i < g->k; i++) member |= g->m[i] == y;
+      if (member || PLAN.pipe[y] == g->pipe) continue;
+      if (!(g->mem + PLAN.mem[y] <= 1.0 - hr + 1e-12)) continue;
+      g->y = y;
+      g->oo = g->ai = g->mj = 0;
+      break;
     }
-    if (wd.keys_out && lane == 0) {
-      wd.keys_out[2 * (serial - wd.shard0)] = cost;
-      wd.keys_out[2 * (serial - wd.shard0) + 1] = fin;
-    }
-    wsync(smask);
+  check : {
+    const double ms = g->oo ? g->mem : PLAN.mem[g->y];
+    if (memgrid(g->mj) + ms > 1.0 - hr + kEps) continue;
+    g->fa = g->oo ? g->y : PLAN.M;
+    g->fb = g->oo ? PLAN.M : g->y;
+    g->falloc = 1 + g->ai * 4 + g->mj;
+    return true;
   }
+  }
+}
+
+// The candidate loop of one group, flattened so that one iteration is one
+// simulated event for every group of the warp (pass and candidate
+// boundaries are short divergent prologues).
+template <int G, int WPL>
+RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm, SliceOut* out) {
+  Lane<G, WPL> S(gbase, lane, gm);
+  S.dbg = wd.dbg;
+  S.dbg_flag = wd.dbg_flag;
+  GroupCand* g = S.gc();
   if (lane == 0) {
-    out->k0 = b0;
-    out->k1 = b1;
-    out->k2 = b2;
-    out->passes = passes;
-    out->bytes = bytes;
-    out->cands = ncand;
+    g->b0 = g->b1 = g->b2 = ~0ull;
+    g->passes = g->ncand = 0;
+    g->bytes = 0.0;
+    g->cls = -1;
+  }
+  gsync<G>(gm);
+  const int64_t total = wd.na + wd.nb + wd.nc;
+  bool active = false;  // a pass is running
+  bool pair = false;
+  int variant = 0, nwin = 0;
+  for (;;) {
+    if (!active) {
+      // ---- pass boundary: fold the finished pass, pick the next one
+      bool more = false;
+      if (g->cls >= 0) {
+        const double x = S.any_done ? S.last : S.now;
+        gsync<G>(gm);
+        if (lane == 0) {
+          if (x < g->cost) g->cost = x;
+          more = next_action(g);
+        }
+        more = gbcast<G>(gm, more ? 1 : 0) != 0;
+      }
+      if (!more) {
+        if (g->cls >= 0 && lane == 0) {  // finished candidate: key (cost, finish, priority, serial)
+          if (S.err) at_cas(wd.err, 0, S.err);
+          g->ncand++;
+          const unsigned long long k0 = dbits(g->cost), k1 = dbits(g->fin);
+          const unsigned long long k2 = ((unsigned long long)g->cls << 61) | (unsigned long long)g->serial;
+          if (key_less(k0, k1, k2, g->b0, g->b1, g->b2)) {
+            g->b0 = k0;
+            g->b1 = k1;
+            g->b2 = k2;
+          }
+          if (wd.keys_out) {
+            wd.keys_out[2 * (g->serial - wd.shard0)] = g->cost;
+            wd.keys_out[2 * (g->serial - wd.shard0) + 1] = g->fin;
+          }
+        }
+        // ---- next candidate (heaviest class first)
+        long long idx = 0;
+        if (lane == 0) {
+          idx = (long long)at_add64(wd.counter, 1ull);
+          if (*(volatile int*)wd.err) idx = total;
+        }
+        idx = gbcast<G>(gm, idx);
+        if (idx >= total) break;
+        if (lane == 0) {
+          const int64_t serial = idx < wd.na ? wd.a0 + idx
+                                             : (idx < wd.na + wd.nb ? wd.b0 + (idx - wd.na) : wd.c0 + (idx - wd.na - wd.nb));
+          Cand c;
+          decode_serial(PLAN, serial, c);
+          g->serial = serial;
+          g->cls = c.cls;
+          g->cost = INFINITY;
+          g->v = 0;
+          g->phase = 0;
+          if (c.cls == 1) {
+            setup_merge(c, g, wd.err);
+            g->fin = (PLAN.now + g->pre) + g->dur;
+            g->nwin = PLAN.NWIN - c.k + 1;
+            g->rm = PLAN.mask0[1 * PLAN.W + g->t];
+            if (g->idle) {  // first pass: Exclusive(M)
+              g->fa = PLAN.M;
+              g->fb = -1;
+              g->falloc = 0;
+            }
+          } else {
+            // action_finish_estimate :773-789 (with the realloc penalty of the decision state)
+            g->a = c.a;
+            g->b = c.cls == 0 ? c.b : -1;
+            g->alloc = c.alloc;
+            g->nwin = PLAN.NWIN;
+            auto pre_of = [&](int n, int alloc) {
+              double pre = PLAN.mprefix[n];
+              if (PLAN.has_penalty && PLAN.kind[n] <= RLX_KIND_DECODE_SMALL) {
+                const double gr = PLAN.grant0[PLAN.worker[n] * PLAN.P + PLAN.pipe[n]];
+                if (!isnan(gr) && fabs(gr - PLAN.alloc_mem[alloc]) > kEps) pre = pre + PLAN.realloc_penalty;
+              }
+              return pre;
+            };
+            if (c.cls == 2) {
+              const double r = S.L3(PLAN.kind[c.a], -1, 0);
+              g->fin = (PLAN.now + pre_of(c.a, 0)) + PLAN.dur[c.a] * r;
+            } else {
+              const double ra = S.L3(PLAN.kind[c.a], PLAN.kind[c.b], c.alloc);
+              const double rbv = S.L3(PLAN.kind[c.b], PLAN.kind[c.a], c.alloc + 12);
+              const double fa = (PLAN.now + pre_of(c.a, c.alloc)) + PLAN.dur[c.a] * ra;
+              const double fb = (PLAN.now + pre_of(c.b, c.alloc + 12)) + PLAN.dur[c.b] * rbv;
+              g->fin = fb > fa ? fb : fa;
+            }
+          }
+        }
+        gsync<G>(gm);
+      }
+      // ---- start the pass
+      const bool is_merge = g->cls == 1;
+      variant = g->v;
+      pair = variant == 1;
+      nwin = g->nwin;
+      Act act;
+      if (!is_merge) {
+        act = Act{g->cls, g->a, g->b, g->alloc};
+      } else if (!g->idle) {
+        act = Act{-1, -1, -1, 0};
+      } else if (g->phase == 0) {
+        act = Act{2, PLAN.M, -1, 0};
+      } else {
+        act = Act{0, g->fa, g->fb, g->falloc};
+      }
+      S.init_pass(variant, act, is_merge);
+      if (lane == 0 && variant == 0) {  // the reference's 3 passes of this action (SURVEY §8(d) bytes)
+        g->passes += 3;
+        g->bytes += 3.0 * (32.0 * nwin + 4.0 * (double)PLAN.ew +
+                           32.0 * (PLAN.n_run0 + (act.cls < 0 ? 0 : act.cls == 0 ? 2 : 1)) + 16.0 * PLAN.n_tw_run0);
+      }
+      active = nwin > 0;
+      if (!active) continue;  // empty window: the pass result is `now` (:889-890)
+    }
+    active = S.step(pair, nwin, g->serial, variant);
+  }
+  if (S.err) at_cas(wd.err, 0, S.err);
+  gsync<G>(gm);
+  if (lane == 0) {
+    out->k0 = g->b0;
+    out->k1 = g->b1;
+    out->k2 = g->b2;
+    out->passes = g->passes;
+    out->bytes = g->bytes;
+    out->cands = g->ncand;
   }
 }
 
-
-template <int L, int WPL>
-__global__ void __launch_bounds__(256, 2) rlx_score_kernel(const WorkDesc wd, SliceOut* outs) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  double* lut = reinterpret_cast<double*>(smem);
-  for (int i = threadIdx.x; i < kLutN; i += blockDim.x) lut[i] = PLAN.lut[i];
+// ---- TMA bulk staging of the hot plan region into shared memory
+__device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
+#ifdef __CUDA_ARCH__
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 1u << 16;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t n = bytes - off < kChunk ? bytes - off : kChunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d + off),
+          "l"(src + off), "r"(n), "r"(b)
+          : "memory");
+    }
+  }
   __syncthreads();
-  const int lane = threadIdx.x % L;
-  const int slice = threadIdx.x / L;
-  const int wl = threadIdx.x & 31;
-  const unsigned smask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (wl / L * L));
-  uint8_t* base = smem + ((kLutN * 8 + 15) & ~15) + (size_t)slice * wd.slice_bytes;
-  slice_loop<L, WPL>(wd, lut, base, lane, smask, &outs[blockIdx.x * (blockDim.x / L) + slice]);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b)
+        : "memory");
+  }
+#endif
 }
 
-// Shard winner + stats over all slices (deterministic: lexicographic min).
+template <int G, int WPL>
+__global__ void __launch_bounds__(512, 1) rlx_score_kernel(const WorkDesc wd, SliceOut* outs) {
+  __shared__ __align__(8) uint64_t bar;
+  stage_hot(rlx_smem, c_plan.hot, c_plan.hot_bytes, &bar);
+  const int lane = threadIdx.x % G;
+  const int grp = threadIdx.x / G;
+  const int wl = threadIdx.x & 31;
+  const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl / G * G));
+  group_loop<G, WPL>(wd, c_plan.hot_bytes + (uint32_t)grp * c_plan.g_bytes, lane, gm,
+                     &outs[blockIdx.x * (blockDim.x / G) + grp]);
+}
+
+// Shard winner + stats over all groups (deterministic: lexicographic min).
 __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long long* res /* 8 words */) {
   __shared__ unsigned long long s0[256], s1[256], s2[256], sp[256], sc[256];
   __shared__ double sb[256];
@@ -839,12 +1057,16 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
     cs += outs[i].cands;
     by += outs[i].bytes;
   }
-  s0[threadIdx.x] = b0; s1[threadIdx.x] = b1; s2[threadIdx.x] = b2;
-  sp[threadIdx.x] = ps; sc[threadIdx.x] = cs; sb[threadIdx.x] = by;
+  s0[threadIdx.x] = b0;
+  s1[threadIdx.x] = b1;
+  s2[threadIdx.x] = b2;
+  sp[threadIdx.x] = ps;
+  sc[threadIdx.x] = cs;
+  sb[threadIdx.x] = by;
   __syncthreads();
   for (int st = blockDim.x / 2; st > 0; st >>= 1) {
     if ((int)threadIdx.x < st) {
-      int o = threadIdx.x + st;
+      const int o = threadIdx.x + st;
       if (key_less(s0[o], s1[o], s2[o], s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x])) {
         s0[threadIdx.x] = s0[o];
         s1[threadIdx.x] = s1[o];
@@ -870,83 +1092,68 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from rlx_abi.cu)
 
-size_t slice_bytes(const DevPlan& P) {
-  size_t b = (sizeof(SliceCand) + 15) & ~size_t(15);
-  b += 8 * (size_t)P.W + 8 * (size_t)P.NTW + (P.has_penalty ? 8 * (size_t)P.W * P.P : 0);
-  b += 4 * (size_t)P.NT + 2 * (size_t)(P.NTW + 8);
-  return (b + 15) & ~size_t(15);
-}
-
-size_t lut_bytes() { return ((size_t)kLutN * 8 + 15) & ~size_t(15); }
-
 typedef void (*KernelFn)(const WorkDesc, SliceOut*);
 
-static KernelFn pick(int L, int WPL) {
-#ifdef RLX_ONLY_32_2
-  return rlx_score_kernel<32, 2>;
+// Lane-group shape for W simulated workers: WPL workers per lane in
+// registers, G = the smallest power of two with G * WPL >= W.
+#ifndef RLX_WPL
+#define RLX_WPL 4
 #endif
-#ifdef RLX_DEBUG_SHAPES
-  // development builds only (librlx_dbg.so): lane-count sweeps for bisecting
-  if (L == 4 && WPL == 8) return rlx_score_kernel<4, 8>;
-  if (L == 8 && WPL == 4) return rlx_score_kernel<8, 4>;
-  if (L == 16 && WPL == 2) return rlx_score_kernel<16, 2>;
-#endif
-  if (L == 4) return rlx_score_kernel<4, 1>;
-  if (L == 8) return rlx_score_kernel<8, 1>;
-  if (L == 16) return rlx_score_kernel<16, 1>;
-  if (WPL == 1) return rlx_score_kernel<32, 1>;
-  if (WPL == 2) return rlx_score_kernel<32, 2>;
-  return rlx_score_kernel<32, 4>;
+void choose_shape(int W, int& G, int& WPL) {
+  WPL = RLX_WPL;
+  G = 1;
+  while (G * WPL < W) G *= 2;
 }
 
-void choose_shape(int W, int& L, int& WPL) {
-  if (W <= 4) L = 4, WPL = 1;
-  else if (W <= 8) L = 8, WPL = 1;
-  else if (W <= 16) L = 16, WPL = 1;
-  else if (W <= 32) L = 32, WPL = 1;
-  else if (W <= 64) L = 32, WPL = 2;
-  else L = 32, WPL = 4;
+static KernelFn pick(int G, int WPL) {
+  if (WPL != RLX_WPL) return nullptr;
+  switch (G) {
+    case 1: return rlx_score_kernel<1, RLX_WPL>;
+    case 2: return rlx_score_kernel<2, RLX_WPL>;
+    case 4: return rlx_score_kernel<4, RLX_WPL>;
+    case 8: return rlx_score_kernel<8, RLX_WPL>;
+    case 16: return rlx_score_kernel<16, RLX_WPL>;
+#if RLX_WPL < 8
+    case 32: return rlx_score_kernel<32, RLX_WPL>;
+#endif
+    default: return nullptr;
+  }
 }
 
-// Returns 0 on success; fills grid/block/smem.
 int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, int sm_count, cudaStream_t st,
                  int* n_slices_out, int threads_hint) {
-  int L, WPL;
-  choose_shape(P.W, L, WPL);
-#ifdef RLX_DEBUG_SHAPES
-  if (const char* sh = getenv("RLX_SHAPE")) sscanf(sh, "%d,%d", &L, &WPL);
-#endif
-  KernelFn fn = pick(L, WPL);
-  size_t sb = slice_bytes(P);
-  wd.slice_bytes = (int)sb;
-  int threads = threads_hint > 0 ? threads_hint : 256;
-  size_t smem = 0;
-  for (;;) {
-    smem = lut_bytes() + (size_t)(threads / L) * sb;
-    if (smem <= 200 * 1024 || threads <= L) break;
-    threads /= 2;
-  }
-  if (smem > 227 * 1024) return RLX_ERR_LIMIT;
+  int G, WPL;
+  choose_shape(P.W, G, WPL);
+  if (const char* sh = getenv("RLX_SHAPE")) sscanf(sh, "%d,%d", &G, &WPL);
+  KernelFn fn = pick(G, WPL);
+  if (!fn || G * WPL < P.W) return RLX_ERR_LIMIT;
+  DevPlan P2 = P;
+  group_layout(P2, G, WPL);
+  const size_t gb = P2.g_bytes;
+  wd.slice_bytes = (int)gb;
+  const size_t hot = P.hot_bytes;
+  const size_t cap = 227 * 1024 - 64;
+  if (hot + gb > cap) return RLX_ERR_LIMIT;
+  int threads = threads_hint > 0 ? threads_hint : 512;
+  while (threads > G && hot + (size_t)(threads / G) * gb > cap) threads /= 2;
+  const size_t smem = hot + (size_t)(threads / G) * gb;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return RLX_ERR_CUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return RLX_ERR_CUDA;
-  if (per_sm < 1) per_sm = 1;
-  int64_t total = wd.na + wd.nb + wd.nc;
-  int64_t need = (total + (threads / L) - 1) / (threads / L);
+  if (per_sm < 1) return RLX_ERR_LIMIT;
+  const int64_t total = wd.na + wd.nb + wd.nc;
+  const int64_t per_block = threads / G;
+  const int64_t need = (total + per_block - 1) / per_block;
   int64_t blocks = (int64_t)per_sm * sm_count;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  int64_t slices = blocks * (threads / L);
-  if (slices > max_slices) {
-    blocks = max_slices / (threads / L);
-    slices = blocks * (threads / L);
-  }
-  if (cudaMemcpyToSymbolAsync(c_plan, &P, sizeof(DevPlan), 0, cudaMemcpyHostToDevice, st) != cudaSuccess)
+  if (blocks * per_block > max_slices) blocks = max_slices / per_block;
+  if (cudaMemcpyToSymbolAsync(c_plan, &P2, sizeof(DevPlan), 0, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return RLX_ERR_CUDA;
   fn<<<(unsigned)blocks, threads, smem, st>>>(wd, outs);
   if (cudaGetLastError() != cudaSuccess) return RLX_ERR_CUDA;
-  *n_slices_out = (int)slices;
+  *n_slices_out = (int)(blocks * per_block);
   return 0;
 }
 

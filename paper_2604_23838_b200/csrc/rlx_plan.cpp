@@ -449,17 +449,52 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   }
   soff[NT] = (int32_t)sl.size();
 
-  // ---- blob
+  // ---- readiness counters: only nodes (and joins) waiting on >= 2 predecessors
+  // need one; a node with a single unresolved predecessor becomes ready when
+  // that predecessor completes.
+  std::vector<uint16_t> ctr_idx(NT, 0xFFFF), ctr0;
+  for (int u = 0; u < NT; u++)
+    if (pend0[u] >= 2) {
+      ctr_idx[u] = (uint16_t)ctr0.size();
+      ctr0.push_back(pend0[u]);
+    }
+  d.NC = (int32_t)ctr0.size();
+  // Variants 0 (suffix key) and 2 (name key) of _complete_window (:875) run
+  // identical simulations when every worker's two orders coincide.
+  d.same_order = 1;
+  for (int w = 0; w < W && d.same_order; w++)
+    for (int q = 0; q < ordcnt[w]; q++)
+      if (ord[(0 * W + w) * kMaxPos + q] != ord[(1 * W + w) * kMaxPos + q]) {
+        d.same_order = 0;
+        break;
+      }
+  int max_ord = 0;
+  for (int w = 0; w < W; w++) max_ord = std::max(max_ord, (int)ordcnt[w]);
+  d.max_ord = max_ord;
+
+  // ---- blob: the hot region (staged into shared memory) comes first
   Blob& B = hp.blob;
   B.buf.clear();
   PlanLayout& L = hp.lay;
+  L.lut = B.put(in->lut, sizeof(double) * RLX_NKIND * RLX_NPARTNER * RLX_NALLOC);
+  L.alloc_mem = B.put(in->alloc_mem, sizeof(double) * RLX_NALLOC);
+  L.dur = B.putv(dur);
+  L.mem = B.putv(mem);
+  L.mprefix = B.putv(mpre);
+  L.succ_off = B.putv(soff);
+  L.ord = B.putv(ord);
   L.kind = B.putv(kind);
   L.pipe = B.putv(pipe);
   L.worker = B.putv(worker);
   L.flags = B.putv(flags);
-  L.dur = B.putv(dur);
-  L.mem = B.putv(mem);
-  L.mprefix = B.putv(mpre);
+  L.pos = B.putv(pos);
+  L.tw_slot = B.putv(twslot);
+  L.tw_node = B.putv(twnode);
+  L.ctr_idx = B.putv(ctr_idx);
+  L.succ = B.putv(sl);
+  L.hot_end = (B.buf.size() + 15) & ~size_t(15);
+  B.buf.resize(L.hot_end);
+  L.ctr0 = B.putv(ctr0);
   L.suffix = B.putv(lsuf);
   L.msx = B.putv(lmsx);
   L.migc = B.putv(migc);
@@ -469,13 +504,7 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.lt_merge = B.putv(ltm);
   L.id_off = B.putv(idoff);
   L.ids = B.putv(ids);
-  L.pos = B.putv(pos);
-  L.tw_slot = B.putv(twslot);
-  L.tw_node = B.putv(twnode);
-  L.succ_off = B.putv(soff);
-  L.succ = B.putv(sl);
   L.pend0 = B.putv(pend0);
-  L.ord = B.putv(ord);
   L.ord_cnt = B.putv(ordcnt);
   L.mask0 = B.putv(mask0);
   L.nmem0 = B.putv(nmem0);
@@ -491,8 +520,6 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.latency = B.put(in->latency, sizeof(double) * P * 3);
   L.latency_ok = B.put(in->latency_ok, P * 3);
   L.has_spec = B.put(in->has_spec, P);
-  L.lut = B.put(in->lut, sizeof(double) * RLX_NKIND * RLX_NPARTNER * RLX_NALLOC);
-  L.alloc_mem = B.put(in->alloc_mem, sizeof(double) * RLX_NALLOC);
   L.mux_a = B.putv(hp.mux_a);
   L.mux_b = B.putv(hp.mux_b);
   L.mux_alloc = B.putv(hp.mux_alloc);
@@ -561,6 +588,26 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.frags = at<uint16_t>(base, L.frags);
   d.combos = at<uint16_t>(base, L.combos);
   d.binom = at<uint64_t>(base, L.binom);
+  d.ctr_idx = at<uint16_t>(base, L.ctr_idx);
+  d.ctr0 = at<uint16_t>(base, L.ctr0);
+  d.hot = base;
+  d.hot_bytes = (uint32_t)L.hot_end;
+  d.o_kind = (uint32_t)L.kind;
+  d.o_pipe = (uint32_t)L.pipe;
+  d.o_worker = (uint32_t)L.worker;
+  d.o_flags = (uint32_t)L.flags;
+  d.o_pos = (uint32_t)L.pos;
+  d.o_tw_slot = (uint32_t)L.tw_slot;
+  d.o_ctr_idx = (uint32_t)L.ctr_idx;
+  d.o_succ_off = (uint32_t)L.succ_off;
+  d.o_succ = (uint32_t)L.succ;
+  d.o_ord = (uint32_t)L.ord;
+  d.o_dur = (uint32_t)L.dur;
+  d.o_mem = (uint32_t)L.mem;
+  d.o_mprefix = (uint32_t)L.mprefix;
+  d.o_lut = (uint32_t)L.lut;
+  d.o_alloc_mem = (uint32_t)L.alloc_mem;
+  d.o_tw_node = (uint32_t)L.tw_node;
 }
 
 }  // namespace rlx

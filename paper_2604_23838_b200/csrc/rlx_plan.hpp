@@ -59,6 +59,19 @@ struct DevPlan {
   double now, headroom, realloc_penalty, default_migration_cost;
   int64_t n_mux, n_merge, n_excl, n_total;
   int64_t ew;  // pred edges with both ends in the window (bytes model)
+  int32_t NC;  // readiness counters: nodes (and joins) with >= 2 unresolved preds
+  int32_t max_ord;  // longest per-worker order (ready-mask width)
+  int32_t same_order;  // 1: suffix order == name order on every worker
+
+  // Hot region: the leading `hot_bytes` of the plan blob hold every array the
+  // event loop touches; the kernel stages it into shared memory with TMA bulk
+  // copies and addresses it through these byte offsets.
+  const uint8_t* hot;
+  uint32_t hot_bytes;
+  uint32_t o_kind, o_pipe, o_worker, o_flags, o_pos, o_tw_slot, o_ctr_idx, o_succ_off, o_succ, o_ord, o_dur,
+      o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node;
+  // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
+  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
 
   // per local node (NT unless noted)
   const uint8_t* kind;       // [NL]
@@ -83,6 +96,8 @@ struct DevPlan {
   const int32_t* succ_off;   // [NT+1]
   const uint16_t* succ;
   const uint16_t* pend0;     // [NT] initial pending predecessors (M: 0)
+  const uint16_t* ctr_idx;   // [NT] counter slot of a node with pend0 >= 2, else 0xFFFF
+  const uint16_t* ctr0;      // [NC] initial counter values
 
   // per worker
   const uint16_t* ord;       // [2][W][kMaxPos]
@@ -138,6 +153,7 @@ struct WorkDesc {
   int* err;
   int slice_bytes;
   double* dbg;      // device, 16 doubles: first guard failure (serial, variant, now, counters)
+  int* dbg_flag;    // device: 0 until the first failure claims dbg
 };
 
 // Decoded candidate.

@@ -13,6 +13,12 @@ from paper_2604_23838_b200.model import SchedulingError
 
 pytestmark = pytest.mark.gpu
 
+# First-decision candidates on which the reference itself raises
+# SchedulingError (window guard, scheduler.py:866): config 4 serial 84807
+# and config 5 serial 819010 (oracle-confirmed; tests/golden/check_livelock.py
+# re-runs the live reference on them).
+LIVELOCK = {"config4": 84807, "config5": 819010}
+
 
 @pytest.fixture(scope="module")
 def Evaluator():
@@ -56,14 +62,15 @@ def test_golden_candidate_keys(Evaluator, golden_keys, name):
     inst = instance(g["instance"])
     ev = Evaluator(inst)
     st = HostState(inst)
-    if name == "config4":
+    if name in LIVELOCK:
         # The reference livelocks on one merge follow-up of this decision
         # (work_left in (EPS/rate, EPS]: consume stops, finished never
         # holds; scheduler.py:335 vs :609) and raises SchedulingError at
         # the 10,000-advance guard (:866). The device reproduces that, so
         # the sampled keys are scored one serial at a time.
-        with pytest.raises(SchedulingError):
+        with pytest.raises(SchedulingError) as ei:
             ev.decide(st, g["window"], g["max_merge"])
+        assert "did not converge" in str(ei.value)
         for serial, prio, cost, fin in g["keys"]:
             ev.decide(st, g["window"], g["max_merge"], shard=(serial, serial + 1), want_keys=True)
             assert (ev.keys[0, 0], ev.keys[0, 1]) == (cost, fin), (name, serial)
@@ -106,18 +113,26 @@ def _prio(ev, s):
     return 1 if isinstance(a, Merge) else (2 if isinstance(a, Exclusive) else 0)
 
 
-def test_config4_livelock_matches_oracle(Evaluator):
-    """Both the device and the oracle raise on the same livelocking candidate."""
+@pytest.mark.parametrize("cfg,window", [("config4", 3), ("config5", 4)])
+def test_livelock_matches_oracle(Evaluator, cfg, window):
+    """Both the device and the oracle raise on the same livelocking candidate,
+    and the device names it."""
     from oracle.oracle import Oracle, OracleError
 
-    inst = instance("config4")
+    serial = LIVELOCK[cfg]
+    inst = instance(cfg)
     st = HostState(inst)
     ev = Evaluator(inst)
     with pytest.raises(SchedulingError) as ei:
-        ev.decide(st, 3, 3, shard=(84807, 84808))
-    assert "did not converge" in str(ei.value)
-    with pytest.raises(OracleError):
-        Oracle(inst).score(st, 3, 3, serials=[84807])
+        ev.decide(st, window, 3)
+    named = int(str(ei.value).split("serial ")[1].split()[0])
+    for s in sorted({serial, named}):
+        with pytest.raises(SchedulingError):
+            ev.decide(st, window, 3, shard=(s, s + 1))
+        with pytest.raises(OracleError):
+            Oracle(inst).score(st, window, 3, serials=[s])
+    if cfg != "config4":
+        return
     # non-merge candidates of the same decision score normally
     n_mux = ev.count(st, 3, 3)
     ev.decide(st, 3, 3, shard=(0, 64), want_keys=True)
@@ -128,13 +143,34 @@ def test_config4_livelock_matches_oracle(Evaluator):
 
 
 @pytest.mark.parametrize("cfg,window,cap,n_sample", [
-    ("config2", 2, 3, 96), ("config2", 2, None, 24), ("config3", 3, 3, 24), ("config5", 4, 3, 6),
+    ("config2", 2, 3, 96), ("config2", 2, None, 24), ("config3", 3, 3, 24),
 ])
 def test_first_decision_vs_oracle(Evaluator, cfg, window, cap, n_sample):
     inst = instance(cfg)
     ev = Evaluator(inst)
     st = HostState(inst)
     _oracle_sample_check(inst, st, window, cap, n_sample, ev)
+
+
+def test_config5_shards_vs_oracle(Evaluator):
+    """Config 5 (8 pipelines, 64 workers, W=4, 1.06M candidates): random
+    candidates from every class scored on the device one shard at a time
+    match the oracle bit-exactly."""
+    from oracle.oracle import Oracle
+
+    inst = instance("config5")
+    ev = Evaluator(inst)
+    st = HostState(inst)
+    d = ev.decide(st, 4, 3, shard=(0, 0))
+    n_mux, n_merge = d.n_multiplex, d.n_merge
+    rng = np.random.default_rng(5)
+    sample = sorted(set(rng.integers(0, n_mux, 3).tolist()) | set((n_mux + rng.integers(0, n_merge, 2)).tolist())
+                    | {d.n_candidates - 1})
+    sample = [s for s in sample if s != LIVELOCK["config5"]]
+    r = Oracle(inst).score(st, 4, 3, serials=sample, want_keys=True)
+    for s, (oc, of) in zip(sample, r["keys"]):
+        ev.decide(st, 4, 3, shard=(s, s + 1), want_keys=True)
+        assert (ev.keys[0, 0], ev.keys[0, 1]) == (oc, of), s
 
 
 def test_config2_schedule_prefix_vs_oracle(Evaluator):

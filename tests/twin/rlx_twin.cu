@@ -2,8 +2,8 @@
 //
 // TEST INFRASTRUCTURE / DEBUGGING TWIN ONLY: compiled into
 // tests/twin/_build/librlx_twin.so, never into librlx.so and never on the
-// product path. It runs the exact slice algorithm of rlx_kernels.cu with
-// L = 1 lane so that a device result can be reproduced and inspected on a
+// product path. It runs the exact group algorithm of rlx_kernels.cu with
+// G = 1 lane so that a device result can be reproduced and inspected on a
 // CPU (warp primitives resolve to host shims).
 #include <stdio.h>
 
@@ -15,6 +15,7 @@
 
 namespace rlx {
 const DevPlan* g_twin_plan = nullptr;
+uint8_t* g_twin_smem = nullptr;
 }
 
 using namespace rlx;
@@ -33,6 +34,7 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
   relocate(hp, hp.blob.buf.data(), dp);
   g_twin_plan = &dp;
   *n_out = dp.n_total;
+  if (getenv("RLX_TWIN_INFO")) fprintf(stderr, "plan: NL %d NWIN %d W %d NC %d same_order %d hot %u\n", dp.NL, dp.NWIN, dp.W, dp.NC, dp.same_order, dp.hot_bytes);
   if (e < 0 || e > dp.n_total) e = dp.n_total;
   if (b < 0) b = 0;
   if (b > e) b = e;
@@ -48,23 +50,31 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
   clip(dp.n_mux + dp.n_merge, dp.n_total, wd.c0, wd.nc);
   wd.shard0 = b;
   unsigned long long counter = 0;
-  int derr = 0;
+  int derr[8] = {0};
   double dbg[16] = {0};
   wd.counter = &counter;
-  wd.err = &derr;
+  wd.err = &derr[0];
+  wd.dbg_flag = &derr[4];
   wd.keys_out = keys_out;
   wd.dbg = dbg;
-  size_t sb = slice_bytes(dp);
-  wd.slice_bytes = (int)sb;
-  std::vector<uint8_t> smem(sb + 64);
+  if (dp.W > 32) {
+    snprintf(err, errlen, "the host twin runs one lane: at most 32 workers (NL %d NT %d NC %d hot %u max_ord %d NTW %d)",
+             dp.NL, dp.NT, dp.NC, dp.hot_bytes, dp.max_ord, dp.NTW);
+    return RLX_ERR_LIMIT;
+  }
+  group_layout(dp, 1, 32);
+  std::vector<double> smem((dp.hot_bytes + dp.g_bytes) / 8 + 16);
+  memcpy(smem.data(), dp.hot, dp.hot_bytes);  // the kernel stages the hot region the same way
+  g_twin_smem = (uint8_t*)smem.data();
+  wd.slice_bytes = (int)dp.g_bytes;
   SliceOut out;
   memset(&out, 0, sizeof out);
-  slice_loop<1, 128>(wd, dp.lut, smem.data(), 0, 1u, &out);
+  group_loop<1, 32>(wd, dp.hot_bytes, 0, 1u, &out);
   key_out[0] = out.k0;
   key_out[1] = out.k1;
   key_out[2] = out.k2;
   key_out[3] = out.passes;
   if (dbg_out) memcpy(dbg_out, dbg, sizeof dbg);
-  if (derr) snprintf(err, errlen, "device error %d", derr);
-  return derr;
+  if (derr[0]) snprintf(err, errlen, "device error %d", derr[0]);
+  return derr[0];
 }

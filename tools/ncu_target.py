@@ -1,4 +1,7 @@
-"""One warm-up + one measured decision at a config (ncu target)."""
+"""One warm-up + one measured decision at a config (ncu target).
+
+    python tools/ncu_target.py <config> <window> <cap|none> [n_serials]
+"""
 import sys
 
 sys.path.insert(0, "/root/repo")
@@ -10,9 +13,10 @@ from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 cfg = sys.argv[1]
 w = int(sys.argv[2])
 cap = None if sys.argv[3] == "none" else int(sys.argv[3])
+shard = (0, int(sys.argv[4])) if len(sys.argv) > 4 else None
 inst = instance(cfg)
 ev = Evaluator(inst)
 st = HostState(inst)
 for _ in range(2):
-    d = ev.decide(st, w, cap)
+    d = ev.decide(st, w, cap, shard=shard)
 print(cfg, d.n_candidates, d.kernel_ms, d.passes, d.alg_bytes)
