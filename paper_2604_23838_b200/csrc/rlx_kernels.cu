@@ -526,7 +526,22 @@ struct Lane {
           const int q = ffs64(m2) - 1;
           const int y = node_at(w, q);
           if (pipe(y) != px) {
-            paired = best_pair(x, y, first, second, al);
+            if (x != PLAN.M && y != PLAN.M) {  // decision-invariant pair: planner table
+              const int cnt = arr<uint8_t>(PLAN.o_ord_cnt)[w];
+              const uint8_t* po = arr<uint8_t>(PLAN.o_pos) + PLAN.NL;  // name-order positions
+              const int ent =
+                  arr<uint8_t>(PLAN.o_ptab)[arr<uint32_t>(PLAN.o_pt_off)[w] + po[x] * cnt + po[y]];
+              if (ent == 0x60) {
+                err = RLX_ERR_KEY;
+              } else if (ent) {
+                paired = true;
+                al = ent & 31;
+                first = (ent & 0x40) ? y : x;
+                second = (ent & 0x40) ? x : y;
+              }
+            } else {
+              paired = best_pair(x, y, first, second, al);
+            }
             if (paired) m &= ~(1ull << q);
             break;
           }
@@ -553,36 +568,41 @@ struct Lane {
     tl = INFINITY;
     Bits fb = 0;
     double* pr = pres();
+    const bool dpos = dt > kEps;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
 #pragma unroll
       for (int s = 0; s < 2; s++) {
         const Bits bit = Bits(1) << (2 * j + s);
-        if (rb & bit) {
-          double d = dt;
-          double p = 0.0;
-          if (pm & bit) {
-            p = pr[2 * j + s];
-            if (p > kEps) {
-              const double used = d < p ? d : p;
-              p = p - used;
-              d = d - used;
-              pr[2 * j + s] = p;
-            }
+        // slot 1 (the second member of a pair) is rare: branch on it; slot 0
+        // is evaluated branch-free and masked
+        if (s == 1 && !(rb & bit)) continue;
+        const bool on = (rb & bit) != Bits(0);
+        double d = dt;
+        double p = 0.0;
+        bool dp = dpos;
+        if (pm & bit) {
+          p = pr[2 * j + s];
+          if (p > kEps) {
+            const double used = d < p ? d : p;
+            p = p - used;
+            d = d - used;
+            pr[2 * j + s] = p;
+            dp = d > kEps;
           }
-          double wv = wk[j][s];
-          const double r = rt[j][s];
-          if (d > kEps && wv > kEps) {
-            const double q = (r == 1.0) ? d : d / r;
-            const double z = wv - q;
-            wv = z > 0.0 ? z : 0.0;
-            wk[j][s] = wv;
-          }
-          if (p <= kEps && wv * r <= kEps) fb |= bit;
         }
+        double wv = wk[j][s];
+        const double r = rt[j][s];
+        double q = d;
+        if (r != 1.0 && on && dp && wv > kEps) q = d / r;
+        const double z = wv - q;
+        const double nw = z > 0.0 ? z : 0.0;
+        wv = (on && dp && wv > kEps) ? nw : wv;
+        wk[j][s] = wv;
+        if (on && p <= kEps && wv * r <= kEps) fb |= bit;
       }
       const Bits both = Bits(3) << (2 * j);
-      if (fb & both) {
+      if ((fb & both) && (rb & both) != (fb & both)) {
         // a survivor whose partner finished drops to its exclusive speed (:615-621)
 #pragma unroll
         for (int s = 0; s < 2; s++) {
@@ -592,18 +612,17 @@ struct Lane {
             pf &= ~bit;
           }
         }
-        rb &= ~(fb & both);
       }
 #pragma unroll
-      for (int s = 0; s < 2; s++) {  // finish_estimate :328
+      for (int s = 0; s < 2; s++) {  // next finish estimates of the survivors (:328)
         const Bits bit = Bits(1) << (2 * j + s);
-        if (rb & bit) {
-          const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
-          const double fe = (now + p) + wk[j][s] * rt[j][s];
-          tl = fe < tl ? fe : tl;
-        }
+        if (s == 1 && !(rb & bit)) continue;
+        const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
+        const double fe = (now + p) + wk[j][s] * rt[j][s];
+        tl = ((rb & bit) && !(fb & bit) && fe < tl) ? fe : tl;
       }
     }
+    rb &= ~fb;
     const int* nd = nds();
     while (fb) {
       const int i = ffs64(fb) - 1;
@@ -1029,8 +1048,11 @@ __device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint
 #endif
 }
 
+// Threads per CTA: 8 workers per lane need ~150 registers, 4 fit in 128.
+constexpr int threads_for(int WPL) { return WPL >= 8 ? 256 : 512; }
+
 template <int G, int WPL>
-__global__ void __launch_bounds__(512, 1) rlx_score_kernel(const WorkDesc wd, SliceOut* outs) {
+__global__ void __launch_bounds__(threads_for(WPL), 1) rlx_score_kernel(const WorkDesc wd, SliceOut* outs) {
   __shared__ __align__(8) uint64_t bar;
   stage_hot(rlx_smem, c_plan.hot, c_plan.hot_bytes, &bar);
   const int lane = threadIdx.x % G;
@@ -1095,29 +1117,34 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
 typedef void (*KernelFn)(const WorkDesc, SliceOut*);
 
 // Lane-group shape for W simulated workers: WPL workers per lane in
-// registers, G = the smallest power of two with G * WPL >= W.
-#ifndef RLX_WPL
-#define RLX_WPL 4
-#endif
+// registers, G = the smallest power of two with G * WPL >= W. RLX_SHAPE=G,WPL
+// overrides it (tuning).
 void choose_shape(int W, int& G, int& WPL) {
-  WPL = RLX_WPL;
+  WPL = 4;  // measured: 4 workers/lane at 512 threads beats 8 at 256 (profiles/r01_shape_sweep.txt)
   G = 1;
   while (G * WPL < W) G *= 2;
 }
 
 static KernelFn pick(int G, int WPL) {
-  if (WPL != RLX_WPL) return nullptr;
-  switch (G) {
-    case 1: return rlx_score_kernel<1, RLX_WPL>;
-    case 2: return rlx_score_kernel<2, RLX_WPL>;
-    case 4: return rlx_score_kernel<4, RLX_WPL>;
-    case 8: return rlx_score_kernel<8, RLX_WPL>;
-    case 16: return rlx_score_kernel<16, RLX_WPL>;
-#if RLX_WPL < 8
-    case 32: return rlx_score_kernel<32, RLX_WPL>;
-#endif
-    default: return nullptr;
+  if (WPL == 4) {
+    switch (G) {
+      case 1: return rlx_score_kernel<1, 4>;
+      case 2: return rlx_score_kernel<2, 4>;
+      case 4: return rlx_score_kernel<4, 4>;
+      case 8: return rlx_score_kernel<8, 4>;
+      case 16: return rlx_score_kernel<16, 4>;
+      case 32: return rlx_score_kernel<32, 4>;
+    }
+  } else if (WPL == 8) {
+    switch (G) {
+      case 1: return rlx_score_kernel<1, 8>;
+      case 2: return rlx_score_kernel<2, 8>;
+      case 4: return rlx_score_kernel<4, 8>;
+      case 8: return rlx_score_kernel<8, 8>;
+      case 16: return rlx_score_kernel<16, 8>;
+    }
   }
+  return nullptr;
 }
 
 int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, int sm_count, cudaStream_t st,
@@ -1134,7 +1161,7 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
   const size_t hot = P.hot_bytes;
   const size_t cap = 227 * 1024 - 64;
   if (hot + gb > cap) return RLX_ERR_LIMIT;
-  int threads = threads_hint > 0 ? threads_hint : 512;
+  int threads = threads_hint > 0 && threads_hint <= threads_for(WPL) ? threads_hint : threads_for(WPL);
   while (threads > G && hot + (size_t)(threads / G) * gb > cap) threads /= 2;
   const size_t smem = hot + (size_t)(threads / G) * gb;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

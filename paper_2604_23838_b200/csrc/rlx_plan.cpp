@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <string>
 #include <vector>
@@ -292,6 +293,59 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
       }
     }
   }
+  // ---- pair table: _best_pair_action (:803-828) of every ordered pair (x, y)
+  // of window compute nodes of different pipelines on the same worker. It is
+  // decision-invariant, so pairing passes look it up instead of searching the
+  // 24-point orientation x alpha x mem grid. Entry: 0 = no feasible pair,
+  // else 0x80 | (second-is-x) << 6 | alloc; 0x40|0x20 flags a missing LUT row.
+  std::vector<uint32_t> pt_off(W + 1, 0);
+  std::vector<uint8_t> ptab;
+  {
+    const double hr = in->headroom;
+    static const double MGP[4] = {0.20, 0.40, 0.60, 0.80};
+    auto L3 = [&](int k, int partner, int alloc, bool& bad) {
+      double v = in->lut[(k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc];
+      if (std::isnan(v)) bad = true;
+      return v;
+    };
+    auto rerated = [](double da, double sa, double db, double sb) {
+      double na = da * sa, nb = db * sb;
+      if (fabs(na - nb) <= kEps) return na;
+      if (na < nb) return na + (1.0 - na / nb) * db;
+      return nb + (1.0 - nb / na) * da;
+    };
+    for (int w = 0; w < W; w++) {
+      const int cnt = ordcnt[w];
+      pt_off[w] = (uint32_t)ptab.size();
+      ptab.resize(ptab.size() + (size_t)cnt * cnt, 0);
+      for (int px = 0; px < cnt; px++)
+        for (int py = 0; py < cnt; py++) {
+          const int a = ord[(1 * W + w) * kMaxPos + px], b = ord[(1 * W + w) * kMaxPos + py];
+          if (pipe[a] == pipe[b]) continue;
+          if (!(mem[a] + mem[b] <= 1.0 - hr + 1e-12)) continue;
+          double best = INFINITY;
+          int ent = 0;
+          bool bad = false;
+          for (int oo = 0; oo < 2; oo++) {
+            const int f = oo ? b : a, sc2 = oo ? a : b;
+            const double ms = mem[sc2];
+            for (int ai = 0; ai < 3; ai++)
+              for (int mj = 0; mj < 4; mj++) {
+                if (MGP[mj] + ms > 1.0 - hr + kEps) continue;
+                const int al = 1 + ai * 4 + mj;
+                const double e = rerated(dur[f], L3(kind[f], kind[sc2], al, bad), dur[sc2],
+                                         L3(kind[sc2], kind[f], al + 12, bad));
+                if (e < best - kEps) {
+                  best = e;
+                  ent = 0x80 | (oo << 6) | al;
+                }
+              }
+          }
+          ptab[pt_off[w] + (size_t)px * cnt + py] = bad ? 0x60 : (uint8_t)ent;
+        }
+    }
+    pt_off[W] = (uint32_t)ptab.size();
+  }
   // ---- running members at the decision state
   std::vector<uint8_t> nmem0(W, 0), mpart0(2 * W, 0);
   std::vector<uint16_t> mnode0(2 * W, 0);
@@ -491,6 +545,9 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.tw_slot = B.putv(twslot);
   L.tw_node = B.putv(twnode);
   L.ctr_idx = B.putv(ctr_idx);
+  L.pt_off = B.putv(pt_off);
+  L.ord_cnt = B.putv(ordcnt);
+  L.ptab = B.putv(ptab);
   L.succ = B.putv(sl);
   L.hot_end = (B.buf.size() + 15) & ~size_t(15);
   B.buf.resize(L.hot_end);
@@ -505,7 +562,6 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.id_off = B.putv(idoff);
   L.ids = B.putv(ids);
   L.pend0 = B.putv(pend0);
-  L.ord_cnt = B.putv(ordcnt);
   L.mask0 = B.putv(mask0);
   L.nmem0 = B.putv(nmem0);
   L.mnode0 = B.putv(mnode0);
@@ -608,6 +664,9 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.o_lut = (uint32_t)L.lut;
   d.o_alloc_mem = (uint32_t)L.alloc_mem;
   d.o_tw_node = (uint32_t)L.tw_node;
+  d.o_pt_off = (uint32_t)L.pt_off;
+  d.o_ord_cnt = (uint32_t)L.ord_cnt;
+  d.o_ptab = (uint32_t)L.ptab;
 }
 
 }  // namespace rlx

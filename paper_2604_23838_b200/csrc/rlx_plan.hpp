@@ -69,7 +69,7 @@ struct DevPlan {
   const uint8_t* hot;
   uint32_t hot_bytes;
   uint32_t o_kind, o_pipe, o_worker, o_flags, o_pos, o_tw_slot, o_ctr_idx, o_succ_off, o_succ, o_ord, o_dur,
-      o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node;
+      o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab, o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
   uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
 

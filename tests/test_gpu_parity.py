@@ -68,8 +68,9 @@ def test_golden_candidate_keys(Evaluator, golden_keys, name):
         # holds; scheduler.py:335 vs :609) and raises SchedulingError at
         # the 10,000-advance guard (:866). The device reproduces that, so
         # the sampled keys are scored one serial at a time.
+        lo = LIVELOCK[name] - 2000  # a shard holding the livelocking candidate
         with pytest.raises(SchedulingError) as ei:
-            ev.decide(st, g["window"], g["max_merge"])
+            ev.decide(st, g["window"], g["max_merge"], shard=(lo, lo + 4000))
         assert "did not converge" in str(ei.value)
         for serial, prio, cost, fin in g["keys"]:
             ev.decide(st, g["window"], g["max_merge"], shard=(serial, serial + 1), want_keys=True)
@@ -124,7 +125,7 @@ def test_livelock_matches_oracle(Evaluator, cfg, window):
     st = HostState(inst)
     ev = Evaluator(inst)
     with pytest.raises(SchedulingError) as ei:
-        ev.decide(st, window, 3)
+        ev.decide(st, window, 3, shard=None if cfg == "config4" else (serial - 3000, serial + 3000))
     named = int(str(ei.value).split("serial ")[1].split()[0])
     for s in sorted({serial, named}):
         with pytest.raises(SchedulingError):
