@@ -142,18 +142,18 @@ def cpu_sample(inst, state, window, cap, n_total, seconds, seed=0):
     threads = os.cpu_count() or 1
     o = Oracle(inst, nthreads=threads)
     rng = np.random.default_rng(seed)
-    # calibrate on one batch of `threads` candidates, then size the sample
-    first = rng.choice(n_total, size=min(threads, n_total), replace=False)
-    t = time.perf_counter()
-    o.score(state, window, cap, serials=np.sort(first), want_keys=True)
-    dt = time.perf_counter() - t
-    per_batch = max(dt, 1e-6)
-    batches = max(1, min(int(seconds / per_batch), 10_000 // threads))
-    n = min(batches * threads, n_total)
-    sample = np.sort(rng.choice(n_total, size=n, replace=False))
-    t = time.perf_counter()
-    o.score(state, window, cap, serials=sample, want_keys=True)
-    dt = time.perf_counter() - t
+    # one-batch warm-up, then batches of uniformly drawn candidates until
+    # about `seconds` of scoring (every thread busy in every batch)
+    o.score(state, window, cap, serials=np.sort(rng.choice(n_total, size=min(threads, n_total), replace=False)))
+    perm = rng.permutation(n_total) if n_total <= 4_000_000 else rng.choice(n_total, 4_000_000, replace=False)
+    n, dt, batch = 0, 0.0, threads
+    while dt < seconds and n < len(perm):
+        part = np.sort(perm[n:n + batch])
+        t = time.perf_counter()
+        o.score(state, window, cap, serials=part, want_keys=True)
+        dt += time.perf_counter() - t
+        n += len(part)
+        batch = min(batch * 2, 64 * threads)
     return n / dt, n, threads, dt
 
 
@@ -255,7 +255,7 @@ def run_ours(args):
     n_total = d0.n_candidates
     ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kern_ms, bytes_l, passes_l = [], [], []
+    kern_ms, bytes_l, passes_l, events_l = [], [], [], []
     winners = set()
     for i in range(args.warmup):
         table.zero_()
@@ -276,6 +276,7 @@ def run_ours(args):
             kern_ms.append(d.kernel_ms)
             bytes_l.append(d.alg_bytes)
             passes_l.append(d.passes)
+            events_l.append(d.events)
             rows = table.cpu().numpy().view(np.uint64)
             winners.add(unpack(rows[best_row(rows)]))
         torch.cuda.synchronize(dev)
@@ -342,6 +343,8 @@ def run_ours(args):
                      "kernel_ms": statistics.mean(kern_ms), "alg_bytes_per_launch": alg_bytes,
                      "passes_per_launch": statistics.mean(passes_l),
                      "kernel_share_of_step": kernel_avg / ms_per_step},
+        "passes_per_decision": int(passes_l[-1]), "events_per_decision": int(events_l[-1]),
+        "events_per_s": events_l[-1] / (statistics.mean(kern_ms) / 1e3),
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
         "winner": {"cost": winner[0][0], "finish": winner[0][1], "priority": winner[0][2],

@@ -191,6 +191,7 @@ typedef struct RlxDecision {
   int64_t h2d_bytes;             /* plan bytes copied host -> device by this call         */
   int64_t d2h_bytes;             /* result bytes copied device -> host                    */
   int64_t shard_begin, shard_end;/* serial range actually scored                          */
+  int64_t events;                /* simulated events (advances) over all passes           */
 } RlxDecision;
 
 int rlx_abi_version(void);

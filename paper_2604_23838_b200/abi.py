@@ -76,7 +76,7 @@ class RlxDecision(C.Structure):
         ("passes", C.c_int64), ("alg_bytes", C.c_double), ("kernel_ms", C.c_double), ("plan_ms", C.c_double),
         ("n_merge", C.c_int64), ("n_multiplex", C.c_int64), ("n_exclusive", C.c_int64),
         ("device_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-        ("shard_begin", C.c_int64), ("shard_end", C.c_int64),
+        ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("events", C.c_int64),
     ]
 
 

@@ -23,7 +23,8 @@ using namespace rlx;
 namespace {
 
 constexpr int kMaxSlices = 1 << 17;
-constexpr size_t kSliceOutBytes = 48;
+constexpr size_t kSliceOutBytes = 56;
+static_assert(sizeof(rlx::SliceOut) == kSliceOutBytes, "SliceOut layout");
 
 struct Handle {
   int device = 0;
@@ -103,7 +104,7 @@ int rlx_open(int device, void** handle) {
       cudaEventCreate(&h->e2) != cudaSuccess ||
       cudaMalloc(&h->d_outs, kSliceOutBytes * kMaxSlices) != cudaSuccess ||
       cudaMalloc(&h->d_counter, 64) != cudaSuccess || cudaMalloc(&h->d_err, 64) != cudaSuccess ||
-      cudaMalloc(&h->d_res, 64) != cudaSuccess || cudaMallocHost(&h->h_res, 64) != cudaSuccess ||
+      cudaMalloc(&h->d_res, 128) != cudaSuccess || cudaMallocHost(&h->h_res, 128) != cudaSuccess ||
       cudaMalloc(&h->d_dbg, 16 * sizeof(double)) != cudaSuccess) {
     delete h;
     return RLX_ERR_CUDA;
@@ -282,17 +283,17 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   if (rc) return fail(h, rc, "reduce launch failed");
   if (args->dev_key_out)
     CK(cudaMemcpyAsync(args->dev_key_out, h->d_res, 32, cudaMemcpyDeviceToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->h_res, h->d_res, 56, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(h->h_res, h->d_res, 64, cudaMemcpyDeviceToHost, h->stream));
   int herr = 0;
-  CK(cudaMemcpyAsync(&h->h_res[7], h->d_err, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(&h->h_res[8], h->d_err, 4, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  herr = (int)(h->h_res[7] & 0xffffffffu);
+  herr = (int)(h->h_res[8] & 0xffffffffu);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->e0, h->e1);
   out->kernel_ms = ms;
   cudaEventElapsedTime(&ms, h->e2, h->e1);
   out->device_ms = ms;
-  out->d2h_bytes = 60;
+  out->d2h_bytes = 68;
   if (herr) {
     if (herr == RLX_ERR_SCHEDULING) {
       cudaMemcpy(h->h_dbg, h->d_dbg, sizeof h->h_dbg, cudaMemcpyDeviceToHost);
@@ -313,6 +314,7 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   out->key.prio_serial = r[2];
   out->key.valid = r[3];
   out->passes = (int64_t)r[4];
+  out->events = (int64_t)r[7];
   double by;
   memcpy(&by, &r[5], 8);
   out->alg_bytes = by;

@@ -193,7 +193,7 @@ struct GroupCand {
   double cost, fin;           // running candidate_cost and action_finish_estimate
   double bytes;               // SURVEY §8(d) algorithmic bytes scored by this group
   unsigned long long b0, b1, b2;  // best packed key of this group
-  unsigned long long passes, ncand, rm;
+  unsigned long long passes, ncand, rm, events;
   long long serial;
   int kind, pipe, t, k, ins0, ins1, idle, cls;
   int a, b, alloc, nwin;  // candidate action (non-merge)
@@ -885,7 +885,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
   GroupCand* g = S.gc();
   if (lane == 0) {
     g->b0 = g->b1 = g->b2 = ~0ull;
-    g->passes = g->ncand = 0;
+    g->passes = g->ncand = g->events = 0;
     g->bytes = 0.0;
     g->cls = -1;
   }
@@ -902,6 +902,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
         const double x = S.any_done ? S.last : S.now;
         gsync<G>(gm);
         if (lane == 0) {
+          g->events += (unsigned long long)S.guard;
           if (x < g->cost) g->cost = x;
           more = next_action(g);
         }
@@ -1014,6 +1015,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
     out->passes = g->passes;
     out->bytes = g->bytes;
     out->cands = g->ncand;
+    out->events = g->events;
   }
 }
 
@@ -1065,9 +1067,9 @@ __global__ void __launch_bounds__(threads_for(WPL), 1) rlx_score_kernel(const Wo
 
 // Shard winner + stats over all groups (deterministic: lexicographic min).
 __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long long* res /* 8 words */) {
-  __shared__ unsigned long long s0[256], s1[256], s2[256], sp[256], sc[256];
+  __shared__ unsigned long long s0[256], s1[256], s2[256], sp[256], sc[256], se[256];
   __shared__ double sb[256];
-  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull, ps = 0, cs = 0;
+  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull, ps = 0, cs = 0, es = 0;
   double by = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     if (key_less(outs[i].k0, outs[i].k1, outs[i].k2, b0, b1, b2)) {
@@ -1077,6 +1079,7 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
     }
     ps += outs[i].passes;
     cs += outs[i].cands;
+    es += outs[i].events;
     by += outs[i].bytes;
   }
   s0[threadIdx.x] = b0;
@@ -1084,6 +1087,7 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
   s2[threadIdx.x] = b2;
   sp[threadIdx.x] = ps;
   sc[threadIdx.x] = cs;
+  se[threadIdx.x] = es;
   sb[threadIdx.x] = by;
   __syncthreads();
   for (int st = blockDim.x / 2; st > 0; st >>= 1) {
@@ -1096,6 +1100,7 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
       }
       sp[threadIdx.x] += sp[o];
       sc[threadIdx.x] += sc[o];
+      se[threadIdx.x] += se[o];
       sb[threadIdx.x] += sb[o];
     }
     __syncthreads();
@@ -1108,6 +1113,7 @@ __global__ void rlx_reduce_kernel(const SliceOut* outs, int n, unsigned long lon
     res[4] = sp[0];
     res[5] = (unsigned long long)__double_as_longlong(sb[0]);
     res[6] = sc[0];
+    res[7] = se[0];
   }
 }
 

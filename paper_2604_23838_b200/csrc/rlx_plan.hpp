@@ -71,7 +71,7 @@ struct DevPlan {
   uint32_t o_kind, o_pipe, o_worker, o_flags, o_pos, o_tw_slot, o_ctr_idx, o_succ_off, o_succ, o_ord, o_dur,
       o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab, o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
-  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
+  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq, g_rts, g_wks;
 
   // per local node (NT unless noted)
   const uint8_t* kind;       // [NL]
@@ -140,6 +140,7 @@ struct SliceOut {
   unsigned long long passes;
   double bytes;
   unsigned long long cands;
+  unsigned long long events;  // simulated events (advances) over all passes
 };
 
 // Work handed to one scoring launch (one serial shard).

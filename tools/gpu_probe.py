@@ -24,4 +24,5 @@ for k in which:
     print(f"config{k} W={w} cap={cap}: n={d.n_candidates} (mux {d.n_multiplex} merge {d.n_merge} excl {d.n_exclusive})"
           f" best=({d.cost!r}, {d.finish!r}, {d.priority}, {d.serial}) passes={d.passes} bytes={d.alg_bytes:.3e}"
           f" kernel={d.kernel_ms:.2f}ms plan={d.plan_ms:.2f}ms wall1={t1*1e3:.1f}ms wall2={t2*1e3:.1f}ms"
-          f" cand/s={d.n_candidates/(d.kernel_ms/1e3):.3e} GB/s={d.alg_bytes/(d.kernel_ms/1e3)/1e9:.1f}", flush=True)
+          f" cand/s={d.n_candidates/(d.kernel_ms/1e3):.3e} GB/s={d.alg_bytes/(d.kernel_ms/1e3)/1e9:.1f}"
+          f" events={d.events} ev/pass={d.events/max(d.passes,1):.1f} ev/s={d.events/(d.kernel_ms/1e3):.3e}", flush=True)
