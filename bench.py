@@ -168,6 +168,41 @@ def cpu_model():
     return "unknown"
 
 
+def schedule_latency(name, device, cpu=False):
+    """p50 decision latency over a whole look-ahead schedule (SURVEY §8(d):
+    config 1 has 18 decisions, mostly 1-8 candidates, so this measures the
+    fixed per-decision overhead). GPU: the public chooser; cpu=True: the
+    oracle port's chooser (reference arm)."""
+    from paper_2604_23838_b200 import drive
+
+    window, cap, _ = CONFIGS[name]
+    inst = load_instance(name)
+    if cpu:
+        from oracle.oracle import Oracle
+
+        choose = Oracle(inst, nthreads=os.cpu_count() or 1).chooser(window, cap)
+    else:
+        from paper_2604_23838_b200.native import Evaluator
+
+        choose = Evaluator(inst, device=device).chooser(window, cap)
+    lat = []
+
+    def timed(state):
+        t = time.perf_counter()
+        a = choose(state)
+        lat.append((time.perf_counter() - t) * 1e3)
+        return a
+
+    drive(inst, timed, "lookahead", {})  # warm-up
+    lat.clear()
+    t = time.perf_counter()
+    s = drive(inst, timed, "lookahead", {})
+    total = time.perf_counter() - t
+    return {"workload": f"{name} full lookahead_schedule (W={window})", "decisions": len(lat),
+            "actions": len(s.actions), "p50_decision_ms": statistics.median(lat), "max_decision_ms": max(lat),
+            "schedule_s": total}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -187,6 +222,7 @@ def run_reference(args):
         if i >= args.warmup:
             rates.append(r)
         last = r
+    sched = schedule_latency(args.schedule_config, 0, cpu=True) if args.schedule_p50 else None
     tot_n = sum(r[1] for r in rates)
     tot_s = sum(r[3] for r in rates)
     value = tot_n / tot_s
@@ -202,6 +238,8 @@ def run_reference(args):
                                    f"per step, scored by oracle/rlx_oracle.c on {last[2]} threads ({cpu_model()})"},
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if sched is not None:
+        line["schedule"] = sched
     print(json.dumps(line), flush=True)
     return 0
 
@@ -216,10 +254,17 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
+    # RLX_DIST_BACKEND=gloo runs several ranks on one device (test of the
+    # multi-rank path on a 1-GPU box); the product path is NCCL, one GPU per rank
+    backend = os.environ.get("RLX_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2604_23838_b200.dist import WORDS, best_row, unpack
     from paper_2604_23838_b200.engine import HostState
     from paper_2604_23838_b200.native import Evaluator
@@ -319,6 +364,9 @@ def run_ours(args):
     alg_bytes = statistics.mean(bytes_l)  # rank 0's shard bytes per launch
     achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
     traffic = ncu_traffic(args.config)
+    sched = None
+    if world == 1 and args.schedule_p50:
+        sched = schedule_latency(args.schedule_config, local)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rate, n, threads, secs = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds)
@@ -353,6 +401,8 @@ def run_ours(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if sched is not None:
+        line["schedule"] = sched
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -368,6 +418,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule-config", default="config1", choices=sorted(CONFIGS))
+    ap.add_argument("--no-schedule", dest="schedule_p50", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
