@@ -39,10 +39,11 @@ def _stale(lib: str = None) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
     """Compile librlx.so (or, with debug_shapes, the development variant
     librlx_dbg.so whose lane shape can be forced with RLX_SHAPE=L,WPL)."""
-    lib = LIB_DBG if debug_shapes else LIB
+    lib = out or (LIB_DBG if debug_shapes else LIB)
     if not force and not _stale(lib):
         return lib
     objs = []
@@ -52,6 +53,11 @@ def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False
                "-Xcompiler", "-ffp-contract=off", "-c", os.path.join(CSRC, src), "-o", obj]
         if debug_shapes:
             cmd.insert(1, "-DRLX_DEBUG_SHAPES")
+        for d in defines:
+            cmd.insert(1, "-D" + d)
+        if out or defines:
+            obj = obj + "." + os.path.basename(lib) + ".o"
+            cmd[-1] = obj
         if verbose and src.endswith("kernels.cu"):
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
@@ -63,4 +69,7 @@ def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv, debug_shapes="--debug-shapes" in sys.argv))
+    args = sys.argv[1:]
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force=True, verbose="--verbose" in args, debug_shapes="--debug-shapes" in args, out=out, defines=defs))

@@ -356,16 +356,11 @@ struct Lane {
     }
     const double d = dur(n);
 #pragma unroll
-    for (int jj = 0; jj < WPL; jj++)
-      if (jj == j) {
-        if (s == 0) {
-          wk[jj][0] = d;
-          rt[jj][0] = rate;
-        } else {
-          wk[jj][1] = d;
-          rt[jj][1] = rate;
-        }
-      }
+    for (int jj = 0; jj < WPL; jj++) {  // predicated register select (no per-lane branches)
+      const bool hit = jj == j;
+      wk[jj][s] = hit ? d : wk[jj][s];
+      rt[jj][s] = hit ? rate : rt[jj][s];
+    }
     const Bits bit = Bits(1) << (2 * j + s);
     nds()[2 * j + s] = n;
     rb |= bit;
@@ -1051,10 +1046,19 @@ __device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint
 }
 
 // Threads per CTA: 8 workers per lane need ~150 registers, 4 fit in 128.
-constexpr int threads_for(int WPL) { return WPL >= 8 ? 256 : 512; }
+#ifndef RLX_T8
+#define RLX_T8 256
+#endif
+constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : 512; }
+
+#ifndef RLX_MINB2
+#define RLX_MINB2 1
+#endif
+constexpr int min_blocks_for(int WPL) { return WPL <= 2 ? RLX_MINB2 : 1; }
 
 template <int G, int WPL>
-__global__ void __launch_bounds__(threads_for(WPL), 1) rlx_score_kernel(const WorkDesc wd, SliceOut* outs) {
+__global__ void __launch_bounds__(threads_for(WPL), min_blocks_for(WPL)) rlx_score_kernel(const WorkDesc wd,
+                                                                                          SliceOut* outs) {
   __shared__ __align__(8) uint64_t bar;
   stage_hot(rlx_smem, c_plan.hot, c_plan.hot_bytes, &bar);
   const int lane = threadIdx.x % G;
@@ -1126,13 +1130,28 @@ typedef void (*KernelFn)(const WorkDesc, SliceOut*);
 // registers, G = the smallest power of two with G * WPL >= W. RLX_SHAPE=G,WPL
 // overrides it (tuning).
 void choose_shape(int W, int& G, int& WPL) {
-  WPL = 4;  // measured: 4 workers/lane at 512 threads beats 8 at 256 (profiles/r01_shape_sweep.txt)
+  // measured (profiles/r01_shape_sweep*.txt): 2 workers/lane up to 16
+  // workers (config 2: 8x2 1.01 s vs 4x4 1.20 s), 4 above (config 3: 8x4
+  // 3.56 s vs 16x2 4.25 s); 8+ workers/lane lose occupancy.
+  WPL = W <= 16 ? 2 : 4;
   G = 1;
   while (G * WPL < W) G *= 2;
 }
 
 static KernelFn pick(int G, int WPL) {
-  if (WPL == 4) {
+  if (WPL == 1) {
+    switch (G) {
+      case 8: return rlx_score_kernel<8, 1>;
+      case 16: return rlx_score_kernel<16, 1>;
+      case 32: return rlx_score_kernel<32, 1>;
+    }
+  } else if (WPL == 2) {
+    switch (G) {
+      case 8: return rlx_score_kernel<8, 2>;
+      case 16: return rlx_score_kernel<16, 2>;
+      case 32: return rlx_score_kernel<32, 2>;
+    }
+  } else if (WPL == 4) {
     switch (G) {
       case 1: return rlx_score_kernel<1, 4>;
       case 2: return rlx_score_kernel<2, 4>;

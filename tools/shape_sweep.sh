@@ -1,6 +1,6 @@
 # lane-group shape sweep of the first decision (development aid)
 export PYTHONDONTWRITEBYTECODE=1
-for sh in 4,4 8,4; do RLX_SHAPE=$sh timeout 120 python tools/gpu_probe.py 2 2>&1 | sed "s/^/[$sh] /" | cut -c1-20,160-420; done
-for sh in 8,4 16,4; do RLX_SHAPE=$sh timeout 120 python tools/gpu_probe.py 3 2>&1 | sed "s/^/[$sh] /" | cut -c1-20,160-420; done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rlx_score -s 1 -c 1 -o gpurun_out/prof_cfg2_v5 -f \
-    python tools/ncu_target.py config2 2 none 60000 > gpurun_out/ncu_full.log 2>&1
+MB=$PWD/paper_2604_23838_b200/librlx_mb2.so
+for sh in 16,1 8,2; do RLX_LIB=$MB RLX_SHAPE=$sh timeout 120 python tools/gpu_probe.py 2 2>&1 | sed "s/^/[mb2 $sh] /" | cut -c1-24,160-420; done
+for sh in 32,1 16,2; do RLX_LIB=$MB RLX_SHAPE=$sh timeout 120 python tools/gpu_probe.py 3 2>&1 | sed "s/^/[mb2 $sh] /" | cut -c1-24,160-420; done
+for sh in 32,2 16,4; do RLX_LIB=$MB RLX_SHAPE=$sh timeout 300 python tools/gpu_probe.py 4 2>&1 | sed "s/^/[mb2 $sh] /" | cut -c1-24,160-420; done
