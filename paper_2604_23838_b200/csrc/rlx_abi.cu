@@ -277,7 +277,9 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   int n_slices = 0;
   CK(cudaEventRecord(h->e0, h->stream));
   rc = launch_score(dp, wd, (SliceOut*)h->d_outs, kMaxSlices, h->sm_count, h->stream, &n_slices, h->threads_hint);
-  if (rc) return fail(h, rc, rc == RLX_ERR_LIMIT ? "plan does not fit in shared memory" : "kernel launch failed");
+  if (rc)
+    return fail(h, rc, rc == RLX_ERR_LIMIT ? "no kernel shape for this worker count, or the plan does not fit in shared memory"
+                                          : "kernel launch failed");
   CK(cudaEventRecord(h->e1, h->stream));
   rc = launch_reduce((SliceOut*)h->d_outs, n_slices, h->d_res, h->stream);
   if (rc) return fail(h, rc, "reduce launch failed");

@@ -144,6 +144,13 @@ RLX_HD long long gbcast(unsigned m, long long v) {
 #endif
   return v;
 }
+RLX_HD int ffs32(unsigned m) {
+#ifdef __CUDA_ARCH__
+  return __ffs((int)m);
+#else
+  return __builtin_ffs((int)m);
+#endif
+}
 RLX_HD int ffs64(unsigned long long m) {
 #ifdef __CUDA_ARCH__
   return __ffsll((long long)m);
@@ -505,7 +512,7 @@ struct Lane {
       if (lane + G * j < W && !((rb >> (2 * j)) & Bits(3))) idle |= 1u << j;
     unsigned long long* mk = mask();
     while (idle) {
-      const int j = ffs64(idle) - 1;
+      const int j = ffs32(idle) - 1;
       idle &= idle - 1;
       const int w = lane + G * j;
       unsigned long long m = mk[w];
@@ -589,7 +596,9 @@ struct Lane {
         double wv = wk[j][s];
         const double r = rt[j][s];
         double q = d;
-        if (r != 1.0 && on && dp && wv > kEps) q = d / r;
+        // only members of a multiplexed pair divide; keep the IEEE division
+        // sequence a real branch instead of an if-converted one every lane pays
+        if (__builtin_expect(r != 1.0 && on && dp && wv > kEps, 0)) q = d / r;
         const double z = wv - q;
         const double nw = z > 0.0 ? z : 0.0;
         wv = (on && dp && wv > kEps) ? nw : wv;
@@ -620,7 +629,7 @@ struct Lane {
     rb &= ~fb;
     const int* nd = nds();
     while (fb) {
-      const int i = ffs64(fb) - 1;
+      const int i = (sizeof(Bits) == 4 ? ffs32((unsigned)fb) : ffs64(fb)) - 1;
       fb &= fb - 1;
       complete(nd[i], ld);
     }
@@ -630,12 +639,14 @@ struct Lane {
   // while the pass continues; on false `now`/`last`/`any_done` hold the result.
   RLX_HD bool step(bool pair, int nwin, long long serial, int variant) {
     select(pair);
-    const bool mine = rb != Bits(0);
     gsync<G>(gm);
     GroupCand* g = gc();
     const int twr = g->tw_run;
-    if (!gany<G>(gm, mine) && twr == 0) return false;  // has_events
+    // next event time; +inf on every lane means no running member (tl is
+    // the min over this lane's members and tool waits), so with no running
+    // tool wait there are no events left (has_events :590)
     const double t = gmin<G>(gm, tl);
+    if (t == INFINITY && twr == 0) return false;
     if (++guard > 10000) {  // scheduler.py:866-867
       err = RLX_ERR_SCHEDULING;
       if (dbg && lane == 0 && at_cas(dbg_flag, 0, 1) == 0) {
@@ -1147,6 +1158,9 @@ static KernelFn pick(int G, int WPL) {
     }
   } else if (WPL == 2) {
     switch (G) {
+      case 1: return rlx_score_kernel<1, 2>;
+      case 2: return rlx_score_kernel<2, 2>;
+      case 4: return rlx_score_kernel<4, 2>;
       case 8: return rlx_score_kernel<8, 2>;
       case 16: return rlx_score_kernel<16, 2>;
       case 32: return rlx_score_kernel<32, 2>;
