@@ -75,14 +75,16 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config):
-    """dram read+write bytes per scoring launch from the committed ncu capture, or None."""
+def ncu_record(config):
+    """(dram read+write bytes per scoring launch, issue summary) from the
+    committed ncu capture of this workload (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(config)
+            d = json.load(fh)
+        return d.get(config), d.get("issue", {}).get(config)
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -363,7 +365,7 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     alg_bytes = statistics.mean(bytes_l)  # rank 0's shard bytes per launch
     achieved = alg_bytes / (statistics.mean(kern_ms) / 1e3) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic, issue = ncu_record(args.config)
     sched = None
     if world == 1 and args.schedule_p50:
         sched = schedule_latency(args.schedule_config, local)
@@ -391,6 +393,11 @@ def run_ours(args):
                      "kernel_ms": statistics.mean(kern_ms), "alg_bytes_per_launch": alg_bytes,
                      "passes_per_launch": statistics.mean(passes_l),
                      "kernel_share_of_step": kernel_avg / ms_per_step},
+        # the kernel's actual bound: SM instruction issue (SURVEY's HBM byte
+        # model counts window re-reads that shared-memory staging removes)
+        "issue_roofline": None if issue is None else {
+            "bound": "sm_issue", "achieved": issue["sm_inst_issued_pct"], "peak": 100.0, "unit": "% of peak issue",
+            "frac": issue["sm_inst_issued_pct"] / 100.0, "source": issue["source"]},
         "passes_per_decision": int(passes_l[-1]), "events_per_decision": int(events_l[-1]),
         "events_per_s": events_l[-1] / (statistics.mean(kern_ms) / 1e3),
         "gpu_launches": 2 * args.steps,

@@ -1060,7 +1060,10 @@ __device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint
 #ifndef RLX_T8
 #define RLX_T8 256
 #endif
-constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : 512; }
+#ifndef RLX_T2
+#define RLX_T2 512
+#endif
+constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : WPL <= 2 ? RLX_T2 : 512; }
 
 #ifndef RLX_MINB2
 #define RLX_MINB2 1
