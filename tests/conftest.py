@@ -19,3 +19,8 @@ def golden_schedules():
 @pytest.fixture(scope="session")
 def golden_keys():
     return load_gz("keys.json.gz")
+
+
+@pytest.fixture(scope="session")
+def golden_schedules_knobs():
+    return load_gz("schedules_knobs.json.gz")

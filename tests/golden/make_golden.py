@@ -5,6 +5,7 @@ GPU box only reads the committed outputs.
 
     python tests/golden/make_golden.py instances      # config + fixture instances
     python tests/golden/make_golden.py schedules      # full recorded schedules (small instances)
+    python tests/golden/make_golden.py schedules_knobs  # the same with non-default Instance knobs
     python tests/golden/make_golden.py keys [cfg...]  # sampled per-candidate keys at decision 0
 """
 
@@ -84,15 +85,46 @@ _FX_CACHE = {}
 
 def _load_fixture(name):
     if name.startswith("config"):
-        if name not in _FX_CACHE:
-            _FX_CACHE[name] = H.build_config(int(name[6:]))
-        return _FX_CACHE[name]
+        base = name.split("|")[0]
+        if base not in _FX_CACHE:
+            _FX_CACHE[base] = H.build_config(int(base[6:]))
+        inst = _FX_CACHE[base]
+        if name.endswith("|knobs"):
+            inst = H.Instance(graphs=inst.graphs, model=inst.model, headroom=KNOBS["headroom"],
+                              realloc_penalty=KNOBS["realloc_penalty"],
+                              default_migration_cost=KNOBS["default_migration_cost"])
+        return inst
     if not _FX_CACHE.get("_fx"):
         _FX_CACHE["_fx"] = fixture_instances()
     inst = _FX_CACHE["_fx"][name.split("|")[0]]
     if name.endswith("|nomerge"):
         inst = H.Instance(graphs=inst.graphs, model=inst.model, merge_enabled=False)
+    if name.endswith("|knobs"):  # non-default Instance knobs (scheduler.py:117-122)
+        inst = H.Instance(graphs=inst.graphs, model=inst.model, headroom=KNOBS["headroom"],
+                          realloc_penalty=KNOBS["realloc_penalty"],
+                          default_migration_cost=KNOBS["default_migration_cost"])
     return inst
+
+
+# realloc penalty on (:463-470), a default migration cost for spec-less
+# pipelines (:539-542), and a wider memory headroom (feasible, complements)
+KNOBS = {"headroom": 0.1, "realloc_penalty": 0.5, "default_migration_cost": 0.25}
+
+
+def cmd_schedules_knobs():
+    jobs = []
+    for w in (1, 3):
+        jobs.append((f"trap_knobs_w{w}", "trap|knobs", w, None, "lookahead"))
+        jobs.append((f"async_small_knobs_w{w}_cap3", "async_small|knobs", w, 3, "lookahead"))
+    for s in range(0, 100, 3):
+        for w in (1, 3):
+            jobs.append((f"rand{s:03d}_knobs_w{w}", f"rand{s:03d}|knobs", w, None, "lookahead"))
+    for s in range(20):
+        jobs.append((f"mig{s:02d}_knobs_w2", f"mig{s:02d}|knobs", 2, None, "lookahead"))
+    jobs.append(("config1_knobs_w1_cap3", "config1|knobs", 1, 3, "lookahead"))
+    with Pool(8) as pool:
+        res = dict(pool.map(_sched_job, jobs, chunksize=1))
+    _dump(res, "schedules_knobs.json.gz")
 
 
 def cmd_schedules():
@@ -177,6 +209,8 @@ if __name__ == "__main__":
         cmd_instances(rest)
     elif cmd == "schedules":
         cmd_schedules()
+    elif cmd == "schedules_knobs":
+        cmd_schedules_knobs()
     elif cmd == "keys":
         cmd_keys(rest)
     else:

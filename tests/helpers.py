@@ -31,13 +31,18 @@ def instance(name):
     from paper_2604_23838_b200 import load_instance
     from paper_2604_23838_b200.model import Instance
 
-    if name.startswith("config"):
-        if name not in _cache:
-            _cache[name] = load_instance(os.path.join(GOLDEN, "instances", f"{name}.json.gz"))
-        return _cache[name]
-    inst = fixtures()[name.split("|")[0]]
+    base = name.split("|")[0]
+    if base.startswith("config"):
+        if base not in _cache:
+            _cache[base] = load_instance(os.path.join(GOLDEN, "instances", f"{base}.json.gz"))
+        inst = _cache[base]
+    else:
+        inst = fixtures()[base]
     if name.endswith("|nomerge"):
         inst = Instance(graphs=inst.graphs, model=inst.model, merge_enabled=False)
+    if name.endswith("|knobs"):  # tests/golden/make_golden.py KNOBS
+        inst = Instance(graphs=inst.graphs, model=inst.model, headroom=0.1, realloc_penalty=0.5,
+                        default_migration_cost=0.25)
     return inst
 
 

@@ -54,6 +54,28 @@ def test_golden_schedules(Evaluator, golden_schedules):
     assert not bad, f"{len(bad)} mismatching schedules, e.g. {bad[:4]}"
 
 
+def test_golden_schedules_knobs(Evaluator, golden_schedules_knobs):
+    """Realloc penalty, default migration cost and headroom 0.1 on the device."""
+    bad = []
+    ev = None
+    for name, g in sorted(golden_schedules_knobs.items()):
+        inst = instance(g["instance"])
+        if ev is None:
+            ev = Evaluator(inst)
+        else:
+            ev.bind(inst)
+        log = []
+        s = drive(inst, ev.chooser(g["window"], g["max_merge"], log), "lookahead", {})
+        acts = [[t.start, action_to_json(t.action)] for t in s.actions]
+        ok = acts == g["actions"] and [list(d["key"]) for d in log] == [list(d["key"]) for d in g["decisions"]]
+        if ok:
+            rep = simulate(s, inst)
+            ok = (rep.makespan, rep.aggregate_throughput) == (g["makespan"], g["throughput"])
+        if not ok:
+            bad.append(name)
+    assert not bad, bad[:5]
+
+
 @pytest.mark.parametrize("name", ["trap", "async_small", "config1", "config2", "config3", "config4", "config5"])
 def test_golden_candidate_keys(Evaluator, golden_keys, name):
     g = golden_keys.get(name)

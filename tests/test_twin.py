@@ -71,6 +71,19 @@ def test_twin_golden_schedules(Twin, golden_schedules):
     assert not bad, bad[:6]
 
 
+def test_twin_golden_schedules_knobs(Twin, golden_schedules_knobs):
+    bad = []
+    for name in sorted(golden_schedules_knobs)[::3]:
+        g = golden_schedules_knobs[name]
+        inst = instance(g["instance"])
+        log = []
+        s = drive(inst, _twin_chooser(inst, g["window"], g["max_merge"], log), "lookahead", {})
+        acts = [[t.start, action_to_json(t.action)] for t in s.actions]
+        if acts != g["actions"] or [d["key"] for d in log] != [list(d["key"]) for d in g["decisions"]]:
+            bad.append(name)
+    assert not bad, bad[:6]
+
+
 @pytest.mark.parametrize("name", ["trap", "async_small", "config1", "config2", "config3"])
 def test_twin_candidate_keys(Twin, golden_keys, name):
     g = golden_keys[name]
