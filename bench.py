@@ -275,7 +275,11 @@ def run_ours(args):
     inst = load_instance(args.config)
     st = HostState(inst)
     ev = Evaluator(inst, device=local)
-    stream = torch.cuda.current_stream(dev)
+    # one explicit stream for torch ops, NCCL, CUDA events and the library
+    # (torch's default current stream is the legacy NULL stream, which the
+    # library cannot be pointed at: NULL means "the handle's own stream")
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ev.set_stream(stream.cuda_stream)
     part = (rank, world)
     table = torch.zeros((world, WORDS), dtype=torch.int64, device=dev)

@@ -200,9 +200,10 @@ int rlx_load_instance(void* handle, const RlxInstanceDesc* inst);
 int rlx_decide(void* handle, const RlxStateDesc* state, const RlxDecideArgs* args, RlxDecision* out);
 int rlx_decode(void* handle, int64_t serial, RlxAction* out);
 /* Issue all further work of this handle on `cuda_stream` (a cudaStream_t of
- * the handle's device, e.g. the caller's current torch stream, so CUDA
- * events and NCCL calls on that stream order with the scoring kernel);
- * NULL restores the handle's private stream. */
+ * the handle's device, e.g. the caller's torch stream, so CUDA events and
+ * NCCL calls on that stream order with the scoring kernel); NULL restores
+ * the handle's private (non-blocking) stream. To order with the legacy
+ * default stream pass cudaStreamLegacy, not NULL. */
 int rlx_set_stream(void* handle, void* cuda_stream);
 const char* rlx_last_error(void* handle);
 void rlx_close(void* handle);
