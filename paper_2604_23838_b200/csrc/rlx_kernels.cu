@@ -902,8 +902,12 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
   int variant = 0, nwin = 0;
   for (;;) {
     if (!active) {
-      // ---- pass boundary: fold the finished pass, pick the next one
+      // ---- pass boundary: fold the finished pass, pick the next one.
+      // Group-shared candidate state is written by lane 0 only; every read
+      // by the other lanes is separated from those writes by a __syncwarp
+      // (memory ordering, not just a shuffle) — compute-sanitizer racecheck.
       bool more = false;
+      gsync<G>(gm);
       if (g->cls >= 0) {
         const double x = S.any_done ? S.last : S.now;
         gsync<G>(gm);
@@ -913,6 +917,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
           more = next_action(g);
         }
         more = gbcast<G>(gm, more ? 1 : 0) != 0;
+        gsync<G>(gm);
       }
       if (!more) {
         if (g->cls >= 0 && lane == 0) {  // finished candidate: key (cost, finish, priority, serial)
@@ -938,6 +943,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
         }
         idx = gbcast<G>(gm, idx);
         if (idx >= total) break;
+        gsync<G>(gm);  // every lane has read the previous candidate's fields
         if (lane == 0) {
           const int64_t serial = idx < wd.na ? wd.a0 + idx
                                              : (idx < wd.na + wd.nb ? wd.b0 + (idx - wd.na) : wd.c0 + (idx - wd.na - wd.nb));
