@@ -16,7 +16,6 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librlx.so")
-LIB_DBG = os.path.join(HERE, "librlx_dbg.so")
 SOURCES = ("rlx_abi.cu", "rlx_kernels.cu", "rlx_plan.cpp")
 HEADERS = ("rlx_plan.hpp", "rlx_hostplan.hpp")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
@@ -39,11 +38,10 @@ def _stale(lib: str = None) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False, out: str | None = None,
-          defines: tuple = ()) -> str:
-    """Compile librlx.so (or, with debug_shapes, the development variant
-    librlx_dbg.so whose lane shape can be forced with RLX_SHAPE=L,WPL)."""
-    lib = out or (LIB_DBG if debug_shapes else LIB)
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Compile librlx.so. `out`/`defines` build a side variant (tuning
+    experiments, e.g. -DRLX_T2=640); the product is always LIB."""
+    lib = out or LIB
     if not force and not _stale(lib):
         return lib
     objs = []
@@ -51,8 +49,6 @@ def build(force: bool = False, verbose: bool = False, debug_shapes: bool = False
         obj = os.path.join(CSRC, src + (".dbg.o" if debug_shapes else ".o"))
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "-c", os.path.join(CSRC, src), "-o", obj]
-        if debug_shapes:
-            cmd.insert(1, "-DRLX_DEBUG_SHAPES")
         for d in defines:
             cmd.insert(1, "-D" + d)
         if out or defines:
@@ -72,4 +68,4 @@ if __name__ == "__main__":
     args = sys.argv[1:]
     out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
     defs = tuple(a[2:] for a in args if a.startswith("-D"))
-    print(build(force=True, verbose="--verbose" in args, debug_shapes="--debug-shapes" in args, out=out, defines=defs))
+    print(build(force=True, verbose="--verbose" in args, out=out, defines=defs))
