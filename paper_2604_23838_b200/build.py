@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return lib
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + (".dbg.o" if debug_shapes else ".o"))
+        obj = os.path.join(CSRC, src + ".o")
         cmd = [nvcc(), ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xcompiler", "-ffp-contract=off", "-c", os.path.join(CSRC, src), "-o", obj]
         for d in defines:
