@@ -170,7 +170,11 @@ def cpu_model():
     return "unknown"
 
 
-def schedule_latency(name, device, cpu=False):
+class _Enough(Exception):
+    pass
+
+
+def schedule_latency(name, device, cpu=False, max_decisions=None):
     """p50 decision latency over a whole look-ahead schedule (SURVEY §8(d):
     config 1 has 18 decisions, mostly 1-8 candidates, so this measures the
     fixed per-decision overhead). GPU: the public chooser; cpu=True: the
@@ -190,19 +194,35 @@ def schedule_latency(name, device, cpu=False):
     lat = []
 
     def timed(state):
+        if max_decisions is not None and len(lat) >= max_decisions:
+            raise _Enough()
         t = time.perf_counter()
         a = choose(state)
         lat.append((time.perf_counter() - t) * 1e3)
         return a
 
-    drive(inst, timed, "lookahead", {})  # warm-up
+    def run():
+        try:
+            return len(drive(inst, timed, "lookahead", {}).actions)
+        except _Enough:
+            return None
+
+    if max_decisions is None:
+        run()  # warm-up: a whole schedule
+    else:
+        from paper_2604_23838_b200.engine import HostState
+
+        choose(HostState(inst))  # warm-up: the first decision
     lat.clear()
     t = time.perf_counter()
-    s = drive(inst, timed, "lookahead", {})
+    n_actions = run()
     total = time.perf_counter() - t
-    return {"workload": f"{name} full lookahead_schedule (W={window})", "decisions": len(lat),
-            "actions": len(s.actions), "p50_decision_ms": statistics.median(lat), "max_decision_ms": max(lat),
-            "schedule_s": total}
+    what = "full lookahead_schedule" if max_decisions is None else f"first {len(lat)} decisions from t=0"
+    out = {"workload": f"{name} {what} (W={window}, max_merge={cap})", "decisions": len(lat),
+           "p50_decision_ms": statistics.median(lat), "max_decision_ms": max(lat), "schedule_s": total}
+    if n_actions is not None:
+        out["actions"] = n_actions
+    return out
 
 
 def run_reference(args):
@@ -224,7 +244,8 @@ def run_reference(args):
         if i >= args.warmup:
             rates.append(r)
         last = r
-    sched = schedule_latency(args.schedule_config, 0, cpu=True) if args.schedule_p50 else None
+    sched = (schedule_latency(args.schedule_config, 0, cpu=True, max_decisions=args.schedule_decisions)
+             if args.schedule_p50 else None)
     tot_n = sum(r[1] for r in rates)
     tot_s = sum(r[3] for r in rates)
     value = tot_n / tot_s
@@ -372,7 +393,7 @@ def run_ours(args):
     traffic, issue = ncu_record(args.config)
     sched = None
     if world == 1 and args.schedule_p50:
-        sched = schedule_latency(args.schedule_config, local)
+        sched = schedule_latency(args.schedule_config, local, max_decisions=args.schedule_decisions)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         rate, n, threads, secs = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds)
@@ -431,6 +452,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule-config", default="config1", choices=sorted(CONFIGS))
     ap.add_argument("--no-schedule", dest="schedule_p50", action="store_false")
+    ap.add_argument("--schedule-decisions", type=int, default=None,
+                    help="time only the first K decisions (SURVEY §8(d): 16 at configs 3-5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
