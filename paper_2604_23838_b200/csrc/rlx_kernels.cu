@@ -13,12 +13,13 @@
 //    LUT — everything the event loop reads) from HBM into shared memory with
 //    TMA bulk copies (cp.async.bulk + mbarrier complete_tx). All passes of all
 //    candidates on that SM then read the plan from shared memory only.
-//  * A "group" of G lanes (G = 1..16, inside one warp) runs one list-
+//  * A "group" of G lanes (G = 1..32, inside one warp) runs one list-
 //    scheduling pass at a time. Lane l owns the simulated workers
-//    {l, l+G, ...} (WPL = workers per lane) and keeps their running members
-//    (<= 2 per worker: node, rate, work left) in registers; prefixes, ready
-//    masks, readiness counters and tool-wait clocks live in the group's slice
-//    of shared memory.
+//    {l, l+G, ...} (WPL = 2 workers per lane up to 16 workers, else 4;
+//    choose_shape) and keeps their running members (<= 2 per worker: rate,
+//    work left) in registers; node ids, prefixes, ready masks, readiness
+//    counters and tool-wait clocks live in the group's slice of shared
+//    memory. Decision-invariant pairings come from the planner's pair table.
 //  * One loop iteration = one simulated event for every group of the warp:
 //    selection on idle workers (find-first-set over a 64-bit ready mask whose
 //    bit order is the completion key), group min of finish estimates
@@ -111,13 +112,6 @@ RLX_HD void gsync(unsigned m) {
 #ifdef __CUDA_ARCH__
   if (G > 1) __syncwarp(m);
 #endif
-}
-template <int G>
-RLX_HD bool gany(unsigned m, bool x) {
-#ifdef __CUDA_ARCH__
-  if (G > 1) return __any_sync(m, x);
-#endif
-  return x;
 }
 template <int G>
 RLX_HD unsigned gsum(unsigned m, unsigned x) {

@@ -71,7 +71,7 @@ struct DevPlan {
   uint32_t o_kind, o_pipe, o_worker, o_flags, o_pos, o_tw_slot, o_ctr_idx, o_succ_off, o_succ, o_ord, o_dur,
       o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab, o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
-  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq, g_rts, g_wks;
+  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
 
   // per local node (NT unless noted)
   const uint8_t* kind;       // [NL]
@@ -152,7 +152,7 @@ struct WorkDesc {
   double* keys_out; // device, optional
   unsigned long long* counter;
   int* err;
-  int slice_bytes;
+  int slice_bytes;  // shared-memory bytes per group (DevPlan::g_bytes)
   double* dbg;      // device, 16 doubles: first guard failure (serial, variant, now, counters)
   int* dbg_flag;    // device: 0 until the first failure claims dbg
 };
