@@ -55,6 +55,11 @@ CONFIGS = {
                          "long-tail migration, uncapped merges"),
     "config3": (3, 3, "async RL 4 pipelines, 32 simulated GPUs, 4096 heavy-tailed rollouts, depth 3, merge cap 3"),
     "config5": (4, 3, "8 pipelines, 64 simulated GPUs, 64k rollouts, depth 4, merge cap 3"),
+    # the reference itself raises SchedulingError at the cap-3 first decision
+    # of configs 4 and 5 (a livelocking merge follow-up, tests/golden/livelock.json);
+    # cap 2 removes those merges and gives the largest decisions that complete
+    "config4_cap2": (3, 2, "4 agentic pipelines (tool waits), 64 simulated GPUs, 16k rollouts, depth 3, merge cap 2"),
+    "config5_cap2": (4, 2, "8 pipelines, 64 simulated GPUs, 64k rollouts, depth 4, merge cap 2"),
 }
 METRIC = "look-ahead candidates evaluated/sec & p50 decision latency at 1/2/4/8 B200"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -63,7 +68,7 @@ L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 def load_instance(name):
     from paper_2604_23838_b200 import load_instance as li
 
-    return li(os.path.join(ROOT, "tests", "golden", "instances", f"{name}.json.gz"))
+    return li(os.path.join(ROOT, "tests", "golden", "instances", f"{name.split('_')[0]}.json.gz"))
 
 
 def measured_peak():

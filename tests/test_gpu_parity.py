@@ -166,7 +166,8 @@ def test_livelock_matches_oracle(Evaluator, cfg, window):
 
 
 @pytest.mark.parametrize("cfg,window,cap,n_sample", [
-    ("config2", 2, 3, 96), ("config2", 2, None, 24), ("config3", 3, 3, 24),
+    ("config2", 2, 3, 96), ("config2", 2, None, 24), ("config3", 3, 3, 24), ("config4", 3, 2, 16),
+    ("config5", 4, 2, 6),
 ])
 def test_first_decision_vs_oracle(Evaluator, cfg, window, cap, n_sample):
     inst = instance(cfg)

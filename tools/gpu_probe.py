@@ -8,11 +8,11 @@ from helpers import instance  # noqa: E402
 from paper_2604_23838_b200.engine import HostState  # noqa: E402
 from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 
-CFG = {1: (1, None), 2: (2, None), 3: (3, 3), 4: (3, 3), 5: (4, 3)}
+CFG = {1: (1, None), 2: (2, None), 3: (3, 3), 4: (3, 3), 5: (4, 3), 52: (4, 2), 42: (3, 2)}
 which = [int(x) for x in sys.argv[1:]] or [1, 2, 3, 4, 5]
 for k in which:
     w, cap = CFG[k]
-    inst = instance(f"config{k}")
+    inst = instance(f"config{str(k)[0]}")
     ev = Evaluator(inst)
     st = HostState(inst)
     t = time.time()
