@@ -635,7 +635,8 @@ struct Lane {
     select(pair);
     gsync<G>(gm);
     GroupCand* g = gc();
-    const int twr = g->tw_run;
+    const bool has_tw = PLAN.NTW != 0;  // uniform: plans without tool waits skip their bookkeeping
+    const int twr = has_tw ? g->tw_run : 0;
     // next event time; +inf on every lane means no running member (tl is
     // the min over this lane's members and tool waits), so with no running
     // tool wait there are no events left (has_events :590)
@@ -677,7 +678,7 @@ struct Lane {
       if (ex) at_add<G>(&g->tw_run, -ex);
       gsync<G>(gm);
     }
-    if (g->twq_n > 0) {
+    if (has_tw && g->twq_n > 0) {
       gsync<G>(gm);
       if (lane == 0) {
         uint16_t* q = twq();
@@ -1079,8 +1080,16 @@ __global__ void __launch_bounds__(threads_for(WPL), min_blocks_for(WPL)) rlx_sco
   const int grp = threadIdx.x / G;
   const int wl = threadIdx.x & 31;
   const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl / G * G));
-  group_loop<G, WPL>(wd, c_plan.hot_bytes + (uint32_t)grp * c_plan.g_bytes, lane, gm,
-                     &outs[blockIdx.x * (blockDim.x / G) + grp]);
+  SliceOut* out = &outs[blockIdx.x * (blockDim.x / G) + grp];
+  if (c_plan.diag_one_group && wl >= G) {  // diagnostic: one group per warp
+    if (lane == 0) {
+      out->k0 = out->k1 = out->k2 = ~0ull;
+      out->passes = out->cands = out->events = 0;
+      out->bytes = 0.0;
+    }
+    return;
+  }
+  group_loop<G, WPL>(wd, c_plan.hot_bytes + (uint32_t)grp * c_plan.g_bytes, lane, gm, out);
 }
 
 // Shard winner + stats over all groups (deterministic: lexicographic min).
@@ -1198,6 +1207,7 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
   if (!fn || G * WPL < P.W) return RLX_ERR_LIMIT;
   DevPlan P2 = P;
   group_layout(P2, G, WPL);
+  P2.diag_one_group = getenv("RLX_DIAG_ONE_GROUP") != nullptr;  // development diagnostic
   const size_t gb = P2.g_bytes;
   wd.slice_bytes = (int)gb;
   const size_t hot = P.hot_bytes;

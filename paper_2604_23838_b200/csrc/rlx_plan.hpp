@@ -62,6 +62,7 @@ struct DevPlan {
   int32_t NC;  // readiness counters: nodes (and joins) with >= 2 unresolved preds
   int32_t max_ord;  // longest per-worker order (ready-mask width)
   int32_t same_order;  // 1: suffix order == name order on every worker
+  int32_t diag_one_group;  // diagnostic launch: only the first group of every warp works
 
   // Hot region: the leading `hot_bytes` of the plan blob hold every array the
   // event loop touches; the kernel stages it into shared memory with TMA bulk
