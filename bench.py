@@ -379,6 +379,9 @@ def run_ours(args):
                 e2e_ms.append(a0.elapsed_time(a1))
                 wall_ms.append(w)
         last_e2e = ev.last
+        from paper_2604_23838_b200.instance_io import action_to_json
+
+        e2e_action = action_to_json(action)
     clocks = clk.summary()
     sum_ms = max_over_ranks(sum(step_ms))
     ms_per_step = sum_ms / args.steps
@@ -435,6 +438,7 @@ def run_ours(args):
         "winner": {"cost": winner[0][0], "finish": winner[0][1], "priority": winner[0][2],
                    "serial": winner[0][3]} if len(winner) == 1 else [list(w) for w in winner],
         "first_decide_plan_ms": d0.plan_ms,
+        "action": e2e_action,
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu

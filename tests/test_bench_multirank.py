@@ -1,6 +1,7 @@
 """The multi-rank bench path (torchrun, candidate shards, one all-reduce per
-decision) on a 1-GPU box: two ranks share cuda:0 over gloo. Every rank must
-agree on the single-GPU winner of the decision."""
+decision) on a 1-GPU box: 2 or 3 ranks (uneven shards) share cuda:0 over
+gloo. The ranks must agree on the single-GPU winner of the decision, for the
+resident-plan steps and for the public-chooser (e2e) decisions."""
 
 import json
 import os
@@ -29,12 +30,14 @@ def _run(cmd, env):
     return json.loads(lines[0])
 
 
-def test_two_ranks_match_one():
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_ranks_match_one(ranks):
     env = dict(os.environ, RLX_DIST_BACKEND="gloo")
     args = ["bench.py", "--config", "config2", "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-schedule"]
     one = _run([sys.executable] + args, env)
-    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                "--master-addr", "127.0.0.1", "--master-port", str(_port())] + args + ["--gpus", "2"], env)
-    assert two["n_gpus"] == 2
+    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(ranks),
+                "--master-addr", "127.0.0.1", "--master-port", str(_port())] + args + ["--gpus", str(ranks)], env)
+    assert two["n_gpus"] == ranks
     assert two["winner"] == one["winner"]
+    assert two["action"] == one["action"]
     assert two["config"]["candidates_per_decision"] == one["config"]["candidates_per_decision"]
