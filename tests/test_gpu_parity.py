@@ -76,7 +76,8 @@ def test_golden_schedules_knobs(Evaluator, golden_schedules_knobs):
     assert not bad, bad[:5]
 
 
-@pytest.mark.parametrize("name", ["trap", "async_small", "config1", "config2", "config3", "config4", "config5"])
+@pytest.mark.parametrize("name", ["trap", "async_small", "config1", "config2", "config3", "config4", "config5",
+                                  "config2_full"])
 def test_golden_candidate_keys(Evaluator, golden_keys, name):
     g = golden_keys.get(name)
     if g is None:
@@ -100,9 +101,13 @@ def test_golden_candidate_keys(Evaluator, golden_keys, name):
         return
     ev.decide(st, g["window"], g["max_merge"], want_keys=True)
     assert ev.last.n_candidates == g["n_candidates"]
+    d = ev.last
     keys = ev.keys
     for serial, prio, cost, fin in g["keys"]:
         assert (keys[serial, 0], keys[serial, 1]) == (cost, fin), (name, serial)
+    if len(g["keys"]) == g["n_candidates"]:  # every candidate is golden: the winner is their minimum
+        best = min((cost, fin, prio, serial) for serial, prio, cost, fin in g["keys"])
+        assert (d.cost, d.finish, d.priority, d.serial) == best
 
 
 def _oracle_sample_check(inst, st, window, cap, n_sample, ev, seed=0):
