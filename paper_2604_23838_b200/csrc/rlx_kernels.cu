@@ -201,6 +201,7 @@ struct GroupCand {
   int phase, y, oo, ai, mj, v;  // pass iterator
   int fa, fb, falloc;     // follow-up action of the current pass
   int twq_n, tw_run;
+  int dsum;  // window completions of the running pass (plans without tool waits)
   uint16_t m[kMaxMembers];
 };
 
@@ -438,6 +439,7 @@ struct Lane {
     if (lane == 0) {
       g->twq_n = 0;
       g->tw_run = PLAN.n_tw_run0;
+      g->dsum = 0;
     }
     rb = pm = pf = 0;
     tl = INFINITY;
@@ -660,6 +662,20 @@ struct Lane {
     now = t;
     unsigned ld = 0;
     consume(dt, ld);
+    if (!has_tw) {
+      // window completions of this event: the completing lanes add to a
+      // group counter before the barrier every lane needs anyway; a
+      // broadcast read replaces a warp reduction on the critical path
+      if (G > 1 && ld) at_add<G>(&g->dsum, (int)ld);
+      gsync<G>(gm);
+      const int cum = G > 1 ? g->dsum : done_cnt + (int)ld;
+      if (cum != done_cnt) {
+        done_cnt = cum;
+        last = now;
+        any_done = true;
+      }
+      return done_cnt < nwin;
+    }
     gsync<G>(gm);
     // tool waits: expiry (:622-626) and auto-start of ready ones (:421-434)
     if (twr) {

@@ -1,4 +1,3 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 300 python tools/gpu_probe.py 2 2>&1 | sed "s/^/[512] /" | cut -c1-24,170-460
-RLX_THREADS=256 timeout 300 python tools/gpu_probe.py 2 2>&1 | sed "s/^/[256] /" | cut -c1-24,170-460
-RLX_THREADS=128 timeout 300 python tools/gpu_probe.py 2 2>&1 | sed "s/^/[128] /" | cut -c1-24,170-460
+timeout 300 python tools/gpu_probe.py 2 3 52 2>&1 | cut -c1-24,170-460
+timeout 900 compute-sanitizer --tool racecheck --print-limit 5 python tools/sanitize_target.py 2>&1 | tail -3
