@@ -1,3 +1,3 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 300 python tools/gpu_probe.py 2 3 52 2>&1 | cut -c1-24,170-460
-timeout 900 compute-sanitizer --tool racecheck --print-limit 5 python tools/sanitize_target.py 2>&1 | tail -3
+timeout 300 python tools/gpu_probe.py 2 3 2>&1 | sed "s/^/[shfl] /" | cut -c1-24,170-460
+RLX_LIB=$PWD/paper_2604_23838_b200/librlx_smin.so timeout 300 python tools/gpu_probe.py 2 3 2>&1 | sed "s/^/[smem] /" | cut -c1-24,170-460
