@@ -215,7 +215,7 @@ def schedule_latency(name, device, cpu=False, max_decisions=None):
     if max_decisions is None:
         run()  # warm-up: a whole schedule
     else:
-        from paper_2604_23838_b200.engine import HostState
+        from paper_2604_23838_b200.state import State as HostState
 
         choose(HostState(inst))  # warm-up: the first decision
     lat.clear()
@@ -234,7 +234,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2604_23838_b200.engine import HostState
+    from paper_2604_23838_b200.state import State as HostState
 
     window, cap, desc = CONFIGS[args.config]
     inst = load_instance(args.config)
@@ -294,7 +294,7 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     from paper_2604_23838_b200.dist import WORDS, best_row, unpack
-    from paper_2604_23838_b200.engine import HostState
+    from paper_2604_23838_b200.state import State as HostState
     from paper_2604_23838_b200.native import Evaluator
 
     window, cap, desc = CONFIGS[args.config]

@@ -17,6 +17,19 @@
  *                                  global winner after the cross-GPU min-loc)
  *   rlx_set_stream                 order the handle's work on a caller stream
  *   rlx_last_error                 text of the last failure
+ *   rlx_drive                      the whole decision loop `_drive` (:925-950) behind
+ *                                  the ABI: plan -> score -> apply winner -> advance
+ *   rlx_plan_info                  host-only planning of one decision (candidate counts,
+ *                                  capacity checks) — no device needed
+ *
+ * and the reference's mutable execution state `ExecState` (:339-634), held
+ * natively (one RlxState per simulated run; no device needed):
+ *
+ *   rlx_state_create / _clone / _destroy   ExecState(instance, record) / clone()
+ *   rlx_state_apply                 ExecState.apply (:486-515, merge surgery :517-581)
+ *   rlx_state_advance               ExecState.advance(until) (:593-627)
+ *   rlx_state_info / _node / _events / _completion   queries
+ *   rlx_state_snapshot              the RlxStateDesc view rlx_decide consumes
  *
  * All arrays are plain host pointers owned by the caller and only read
  * during the call. Times are IEEE-754 binary64 seconds; every cost/finish
@@ -31,7 +44,7 @@
 extern "C" {
 #endif
 
-#define RLX_ABI_VERSION 2
+#define RLX_ABI_VERSION 3
 
 /* Kind codes = declaration order of rlmux SubStageKind (graph.py:69-76). */
 enum {
@@ -193,6 +206,139 @@ typedef struct RlxDecision {
   int64_t shard_begin, shard_end;/* serial range actually scored                          */
   int64_t events;                /* simulated events (advances) over all passes           */
 } RlxDecision;
+
+/* ---- native execution state (ExecState) ------------------------------ */
+
+/* Static sub-stage graph of an instance: every pipeline graph's nodes in
+ * Instance.graphs order, then each graph's node insertion order (the
+ * reference's ExecState dict order, scheduler.py:348-356). */
+typedef struct RlxGraphDesc {
+  int32_t n_nodes;
+  int32_t n_edges;
+  const int32_t* pipe;           /* [n] pipeline index                                    */
+  const int32_t* worker;         /* [n] dense worker index                                */
+  const int32_t* kind;           /* [n] RLX_KIND_*                                        */
+  const double* duration;
+  const double* mem;
+  const int64_t* remaining;
+  const int64_t* active;
+  const int64_t* context;
+  const int64_t* token_total;
+  const int64_t* span_lo;        /* step_span                                             */
+  const int64_t* span_hi;
+  const char* ids;               /* NUL-separated node ids                                */
+  const int32_t* id_off;
+  const int32_t* edge_src;
+  const int32_t* edge_dst;
+} RlxGraphDesc;
+
+/* One action to apply (node indices are RlxState node indices). Rates are
+ * the slowdown factors of the allocation (SlowdownModel.slowdown); NaN
+ * marks a missing table row, reported as RLX_ERR_KEY after validation, in
+ * the reference's order (scheduler.py:486-505). */
+typedef struct RlxApply {
+  int32_t cls;                   /* RLX_CLASS_*                                           */
+  int32_t node_a, node_b;
+  int32_t target_worker;         /* Merge: dense worker index                             */
+  int32_t n_members;
+  int32_t _pad;
+  int32_t members[RLX_MAX_MEMBERS];
+  double rate_a, rate_b;
+  double sm_a, mem_a, sm_b, mem_b;
+} RlxApply;
+
+typedef struct RlxStateInfo {
+  double now;
+  double makespan;
+  int32_t n_total;               /* node slots (dead merge members included)              */
+  int32_t n_alive;
+  int32_t n_done;
+  int32_t done;
+  int32_t has_events;
+  int32_t n_running;
+  int32_t n_toolwaits;
+  int32_t _pad;
+  int64_t revision;              /* bumped by every merge (structure change)              */
+  int64_t n_events;              /* recorded events (record=1)                            */
+} RlxStateInfo;
+
+typedef struct RlxNodeInfo {
+  int32_t pipe, worker, kind, alive, completed, running;
+  double duration, mem, completion_time;
+  int64_t remaining, active, context, token_total, span_lo, span_hi;
+  const char* id;                /* owned by the state                                    */
+} RlxNodeInfo;
+
+/* Recorded event (scheduler.py:389-391; kinds as rlmux/sim.py:45). */
+enum { RLX_EV_START = 0, RLX_EV_FINISH = 1, RLX_EV_RERATE = 2, RLX_EV_MERGE = 3, RLX_EV_MIGRATION = 4,
+       RLX_EV_TOOLWAIT_START = 5 };
+typedef struct RlxEvent {
+  double time;
+  int32_t worker;                /* dense worker index                                    */
+  int32_t kind;                  /* RLX_EV_*                                              */
+  int32_t node;
+  int32_t _pad;
+  double sm, mem;                /* allocation of start / rerate events (NaN otherwise)   */
+} RlxEvent;
+
+int rlx_state_create(const RlxInstanceDesc* inst, const RlxGraphDesc* graph, int record, void** state);
+int rlx_state_clone(const void* state, void** out);
+void rlx_state_destroy(void* state);
+const char* rlx_state_error(const void* state);
+int rlx_state_apply(void* state, const RlxApply* action);
+int rlx_state_advance(void* state, int has_until, double until);
+int rlx_state_info(const void* state, RlxStateInfo* out);
+/* Fills `out` with views of the state's own arrays, valid until the next
+ * mutation of the state. */
+int rlx_state_snapshot(void* state, RlxStateDesc* out);
+int rlx_state_node(const void* state, int32_t node, RlxNodeInfo* out);
+int rlx_state_events(const void* state, int64_t first, int64_t count, RlxEvent* out);
+int rlx_state_completion(const void* state, uint8_t* completed /* [n_total] */, double* times /* [n_total] */);
+
+/* ---- the whole decision loop behind the ABI --------------------------- */
+
+typedef struct RlxDriveArgs {
+  int32_t window;
+  int32_t max_merge;             /* <= 0: uncapped                                        */
+  int64_t max_decisions;         /* stop after this many chooser calls (<= 0: run to done) */
+  int64_t max_steps;             /* capacity of the `steps` array                         */
+} RlxDriveArgs;
+
+/* One applied action of the schedule (TimedAction) plus its decision. */
+typedef struct RlxStep {
+  double start;                  /* state.now when the action was applied                 */
+  RlxAction action;              /* node indices = RlxState node indices                  */
+  double cost, finish;           /* winning key                                           */
+  int32_t priority;
+  int32_t _pad;
+  int64_t serial;
+  int64_t n_candidates;
+  double decision_ms;            /* host state in -> winner applied (wall clock)          */
+  double kernel_ms;              /* scoring kernel (CUDA events)                          */
+} RlxStep;
+
+/* `_drive(instance, chooser, ...)` (scheduler.py:925-950) with the device
+ * chooser: repeat { plan + score + argmin on the GPU; apply the winner to
+ * `state` } until no candidate, then advance; until the state is done.
+ * Writes the applied actions to `steps` (*n_steps of them) and the number
+ * of chooser calls (decisions with >= 1 candidate) to *n_decisions. On a
+ * failure the steps applied so far stay valid. */
+int rlx_drive(void* handle, void* state, const RlxDriveArgs* args, RlxStep* steps, int64_t* n_steps,
+              int64_t* n_decisions);
+
+/* Host-only planning of one decision (no device, no handle): candidate
+ * counts and the plan's sizes, or the capacity error the device path would
+ * report (RLX_ERR_LIMIT) with its text in `err`. */
+typedef struct RlxPlanInfo {
+  int64_t n_candidates, n_multiplex, n_merge, n_exclusive;
+  int32_t window_nodes;          /* |window| (N_w)                                        */
+  int32_t local_nodes;           /* window + auxiliary tool waits                         */
+  int32_t max_worker_order;      /* longest per-worker ready order (ready-mask bits)      */
+  int32_t hot_bytes;             /* plan bytes staged into shared memory                  */
+  int64_t blob_bytes;            /* plan bytes copied host -> device                      */
+} RlxPlanInfo;
+int rlx_plan_info(const RlxInstanceDesc* inst, const RlxStateDesc* state, int32_t window, int32_t max_merge,
+                  RlxPlanInfo* out, char* err, int32_t err_len);
 
 int rlx_abi_version(void);
 int rlx_open(int device, void** handle);

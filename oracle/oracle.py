@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 from paper_2604_23838_b200 import abi
-from paper_2604_23838_b200.encode import InstanceEncoding, StateEncoding
+from paper_2604_23838_b200.encode import instance_encoding
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "librlx_oracle.so")
@@ -55,8 +55,7 @@ class Oracle:
     """Scores decision states exactly like the reference chooser."""
 
     def __init__(self, instance, nthreads: int | None = None):
-        self.enc = InstanceEncoding(instance)
-        self.senc = StateEncoding(self.enc)
+        self.enc = instance_encoding(instance)
         self.nthreads = nthreads or os.cpu_count() or 1
 
     def score(self, state, window: int, max_merge: int | None = None, serials=None, want_keys=False):
@@ -65,7 +64,7 @@ class Oracle:
         if want_keys and serials is None:
             # the count first: every encode() replaces the arrays an earlier descriptor points into
             n_all = self.score(state, window, max_merge, serials=[], want_keys=False)["n"]
-        sd = self.senc.encode(state)
+        sd = state.snapshot()
         mm = 0 if max_merge is None else int(max_merge)
         ser = None
         nser = 0
@@ -101,7 +100,7 @@ class Oracle:
         return out
 
     def candidate(self, state, serial: int, max_merge: int | None = None):
-        sd = self.senc.encode(state)
+        sd = state.snapshot()
         buf = (C.c_int32 * (6 + abi.RLX_MAX_MEMBERS))()
         err = C.create_string_buffer(256)
         rc = lib().oracle_candidate(C.byref(self.enc.desc), C.byref(sd), 0 if max_merge is None else int(max_merge),
@@ -112,7 +111,7 @@ class Oracle:
         a.cls, a.node_a, a.node_b, a.alloc, a.target_worker, a.n_members = buf[:6]
         for i in range(a.n_members):
             a.members[i] = buf[6 + i]
-        return self.senc.action_from_raw(a)
+        return state.action_from_raw(a)
 
     def chooser(self, window: int, max_merge: int | None = None, log=None):
         """A `drive` chooser that decides with the oracle."""

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-RLX_ABI_VERSION = 2
+RLX_ABI_VERSION = 3
 RLX_F_NO_SYNC_STATS = 1
 RLX_F_REUSE_PLAN = 2
 RLX_F_SHARD = 4
@@ -80,9 +80,76 @@ class RlxDecision(C.Structure):
     ]
 
 
+class RlxGraphDesc(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int32), ("n_edges", C.c_int32),
+        ("pipe", _ip), ("worker", _ip), ("kind", _ip), ("duration", _dp), ("mem", _dp),
+        ("remaining", _lp), ("active", _lp), ("context", _lp), ("token_total", _lp),
+        ("span_lo", _lp), ("span_hi", _lp), ("ids", C.c_char_p), ("id_off", _ip),
+        ("edge_src", _ip), ("edge_dst", _ip),
+    ]
+
+
+class RlxApply(C.Structure):
+    _fields_ = [
+        ("cls", C.c_int32), ("node_a", C.c_int32), ("node_b", C.c_int32), ("target_worker", C.c_int32),
+        ("n_members", C.c_int32), ("_pad", C.c_int32), ("members", C.c_int32 * RLX_MAX_MEMBERS),
+        ("rate_a", C.c_double), ("rate_b", C.c_double),
+        ("sm_a", C.c_double), ("mem_a", C.c_double), ("sm_b", C.c_double), ("mem_b", C.c_double),
+    ]
+
+
+class RlxStateInfo(C.Structure):
+    _fields_ = [
+        ("now", C.c_double), ("makespan", C.c_double),
+        ("n_total", C.c_int32), ("n_alive", C.c_int32), ("n_done", C.c_int32), ("done", C.c_int32),
+        ("has_events", C.c_int32), ("n_running", C.c_int32), ("n_toolwaits", C.c_int32), ("_pad", C.c_int32),
+        ("revision", C.c_int64), ("n_events", C.c_int64),
+    ]
+
+
+class RlxNodeInfo(C.Structure):
+    _fields_ = [
+        ("pipe", C.c_int32), ("worker", C.c_int32), ("kind", C.c_int32), ("alive", C.c_int32),
+        ("completed", C.c_int32), ("running", C.c_int32),
+        ("duration", C.c_double), ("mem", C.c_double), ("completion_time", C.c_double),
+        ("remaining", C.c_int64), ("active", C.c_int64), ("context", C.c_int64), ("token_total", C.c_int64),
+        ("span_lo", C.c_int64), ("span_hi", C.c_int64), ("id", C.c_char_p),
+    ]
+
+
+RLX_EV_START, RLX_EV_FINISH, RLX_EV_RERATE, RLX_EV_MERGE, RLX_EV_MIGRATION, RLX_EV_TOOLWAIT_START = range(6)
+EVENT_NAMES = ("start", "finish", "rerate", "merge", "migration", "toolwait-start")  # rlmux/sim.py:45
+
+
+class RlxEvent(C.Structure):
+    _fields_ = [("time", C.c_double), ("worker", C.c_int32), ("kind", C.c_int32), ("node", C.c_int32),
+                ("_pad", C.c_int32), ("sm", C.c_double), ("mem", C.c_double)]
+
+
+class RlxDriveArgs(C.Structure):
+    _fields_ = [("window", C.c_int32), ("max_merge", C.c_int32), ("max_decisions", C.c_int64),
+                ("max_steps", C.c_int64)]
+
+
+class RlxStep(C.Structure):
+    _fields_ = [("start", C.c_double), ("action", RlxAction), ("cost", C.c_double), ("finish", C.c_double),
+                ("priority", C.c_int32), ("_pad", C.c_int32), ("serial", C.c_int64), ("n_candidates", C.c_int64),
+                ("decision_ms", C.c_double), ("kernel_ms", C.c_double)]
+
+
+class RlxPlanInfo(C.Structure):
+    _fields_ = [("n_candidates", C.c_int64), ("n_multiplex", C.c_int64), ("n_merge", C.c_int64),
+                ("n_exclusive", C.c_int64), ("window_nodes", C.c_int32), ("local_nodes", C.c_int32),
+                ("max_worker_order", C.c_int32), ("hot_bytes", C.c_int32), ("blob_bytes", C.c_int64)]
+
+
 # Every symbol include/rlx.h declares (checked by tests/test_abi.py).
 EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "rlx_decode",
-            "rlx_last_error", "rlx_close", "rlx_set_stream")
+            "rlx_last_error", "rlx_close", "rlx_set_stream", "rlx_drive", "rlx_plan_info",
+            "rlx_state_create", "rlx_state_clone", "rlx_state_destroy", "rlx_state_error", "rlx_state_apply",
+            "rlx_state_advance", "rlx_state_info", "rlx_state_snapshot", "rlx_state_node", "rlx_state_events",
+            "rlx_state_completion")
 
 
 def bind(lib: C.CDLL) -> C.CDLL:
@@ -103,4 +170,33 @@ def bind(lib: C.CDLL) -> C.CDLL:
     lib.rlx_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     lib.rlx_close.restype = None
     lib.rlx_close.argtypes = [C.c_void_p]
+    lib.rlx_drive.restype = C.c_int
+    lib.rlx_drive.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(RlxDriveArgs), C.POINTER(RlxStep),
+                              C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    lib.rlx_plan_info.restype = C.c_int
+    lib.rlx_plan_info.argtypes = [C.POINTER(RlxInstanceDesc), C.POINTER(RlxStateDesc), C.c_int32, C.c_int32,
+                                  C.POINTER(RlxPlanInfo), C.c_char_p, C.c_int32]
+    lib.rlx_state_create.restype = C.c_int
+    lib.rlx_state_create.argtypes = [C.POINTER(RlxInstanceDesc), C.POINTER(RlxGraphDesc), C.c_int,
+                                     C.POINTER(C.c_void_p)]
+    lib.rlx_state_clone.restype = C.c_int
+    lib.rlx_state_clone.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.rlx_state_destroy.restype = None
+    lib.rlx_state_destroy.argtypes = [C.c_void_p]
+    lib.rlx_state_error.restype = C.c_char_p
+    lib.rlx_state_error.argtypes = [C.c_void_p]
+    lib.rlx_state_apply.restype = C.c_int
+    lib.rlx_state_apply.argtypes = [C.c_void_p, C.POINTER(RlxApply)]
+    lib.rlx_state_advance.restype = C.c_int
+    lib.rlx_state_advance.argtypes = [C.c_void_p, C.c_int, C.c_double]
+    lib.rlx_state_info.restype = C.c_int
+    lib.rlx_state_info.argtypes = [C.c_void_p, C.POINTER(RlxStateInfo)]
+    lib.rlx_state_snapshot.restype = C.c_int
+    lib.rlx_state_snapshot.argtypes = [C.c_void_p, C.POINTER(RlxStateDesc)]
+    lib.rlx_state_node.restype = C.c_int
+    lib.rlx_state_node.argtypes = [C.c_void_p, C.c_int32, C.POINTER(RlxNodeInfo)]
+    lib.rlx_state_events.restype = C.c_int
+    lib.rlx_state_events.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(RlxEvent)]
+    lib.rlx_state_completion.restype = C.c_int
+    lib.rlx_state_completion.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_double)]
     return lib

@@ -11,11 +11,13 @@
 #include <string.h>
 
 #include <chrono>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/rlx.h"
 #include "rlx_hostplan.hpp"
+#include "rlx_state.hpp"
 
 
 using namespace rlx;
@@ -42,7 +44,8 @@ struct Handle {
   std::vector<uint8_t> latency_ok, has_spec;
   // plan
   HostPlan hp;
-  bool have_plan = false;
+  bool have_plan = false;      // hp holds the plan of the last decide
+  bool plan_on_device = false; // ... and d_blob holds its copy
   DevPlan host_view{};
   // device buffers
   uint8_t* d_blob = nullptr;
@@ -51,15 +54,15 @@ struct Handle {
   size_t pin_cap = 0;
   uint8_t* d_outs = nullptr;
   unsigned long long* d_counter = nullptr;
-  int* d_err = nullptr;
+  unsigned long long* d_errkey = nullptr;
   unsigned long long* d_res = nullptr;
   unsigned long long* h_res = nullptr;
   double* d_keys = nullptr;
   size_t keys_cap = 0;
-  double* d_dbg = nullptr;
-  double h_dbg[16];
   int threads_hint = 0;
 };
+
+
 
 int fail(Handle* h, int code, const std::string& msg) {
   h->err = msg;
@@ -69,6 +72,29 @@ int fail(Handle* h, int code, const std::string& msg) {
 int cuda_fail(Handle* h, cudaError_t e, const char* where) {
   h->err = std::string(where) + ": " + cudaGetErrorString(e);
   return RLX_ERR_CUDA;
+}
+
+// The scoring kernel reads its plan from one __constant__ symbol per device
+// (rlx_kernels.cu), so two handles on the same device must not interleave
+// "copy plan -> launch -> wait" sequences: one lock per device orders them.
+std::mutex g_device_lock[64];
+
+const char* kind_name(int k) {
+  static const char* names[RLX_NKIND] = {"PrefillBurst", "DecodeLarge", "DecodeMedium", "DecodeSmall",
+                                         "Reference",    "Training",    "ToolWait"};
+  return k >= 0 && k < RLX_NKIND ? names[k] : "?";
+}
+
+// Device error code (rlx_kernels.cu kErr*) -> status + the reference's text.
+int device_error(Handle* h, int code) {
+  if (code == RLX_ERR_SCHEDULING) return fail(h, RLX_ERR_SCHEDULING, "window estimate did not converge");  // :867
+  if (code >= 8 && code < 16) return fail(h, RLX_ERR_KEY, std::to_string(code - 8));  // latency_model[bucket]
+  if (code >= 16) {
+    const int k = (code - 16) / RLX_NPARTNER, p = (code - 16) % RLX_NPARTNER - 1;
+    return fail(h, RLX_ERR_KEY, std::string("slowdown table has no rows for pair ") + kind_name(k) + "/" +
+                                    (p < 0 ? "-" : kind_name(p)));  // slowdown.py:143-147
+  }
+  return fail(h, RLX_ERR_CUDA, "device error " + std::to_string(code));
 }
 
 #define CK(x)                                   \
@@ -103,9 +129,8 @@ int rlx_open(int device, void** handle) {
       cudaEventCreate(&h->e0) != cudaSuccess || cudaEventCreate(&h->e1) != cudaSuccess ||
       cudaEventCreate(&h->e2) != cudaSuccess ||
       cudaMalloc(&h->d_outs, kSliceOutBytes * kMaxSlices) != cudaSuccess ||
-      cudaMalloc(&h->d_counter, 64) != cudaSuccess || cudaMalloc(&h->d_err, 64) != cudaSuccess ||
-      cudaMalloc(&h->d_res, 128) != cudaSuccess || cudaMallocHost(&h->h_res, 128) != cudaSuccess ||
-      cudaMalloc(&h->d_dbg, 16 * sizeof(double)) != cudaSuccess) {
+      cudaMalloc(&h->d_counter, 64) != cudaSuccess || cudaMalloc(&h->d_errkey, 64) != cudaSuccess ||
+      cudaMalloc(&h->d_res, 128) != cudaSuccess || cudaMallocHost(&h->h_res, 128) != cudaSuccess) {
     delete h;
     return RLX_ERR_CUDA;
   }
@@ -157,6 +182,7 @@ int rlx_load_instance(void* handle, const RlxInstanceDesc* in) {
   d.alloc_mem = h->alloc_mem.data();
   h->loaded = true;
   h->have_plan = false;
+  h->plan_on_device = false;
   return RLX_OK;
 }
 
@@ -176,9 +202,7 @@ static void fill_action(Handle* h, const Cand& c, RlxAction* out) {
   }
 }
 
-int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, RlxDecision* out) {
-  Handle* h = (Handle*)handle;
-  if (!h || !args || !out) return RLX_ERR_ARG;
+static int decide_impl(Handle* h, const RlxStateDesc* sd, const RlxDecideArgs* args, RlxDecision* out) {
   if (!h->loaded) return fail(h, RLX_ERR_ARG, "no instance loaded");
   if (args->window < 1) return fail(h, RLX_ERR_VALUE, "window must be >= 1");
   const bool reuse = (args->flags & RLX_F_REUSE_PLAN) != 0;
@@ -191,6 +215,7 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   int rc = 0;
   if (!reuse) {
     h->have_plan = false;
+    h->plan_on_device = false;
     rc = build_plan(&h->inst, sd, args->window, args->max_merge, h->hp, h->err);
     if (rc) return rc;
     h->have_plan = true;
@@ -203,12 +228,10 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   out->n_exclusive = hv.n_excl;
   int64_t b = args->serial_begin < 0 ? 0 : args->serial_begin;
   int64_t e = args->serial_end < 0 ? hv.n_total : args->serial_end;
-  if (args->flags & RLX_F_SHARD) {  // contiguous block `serial_begin` of `serial_end` blocks
+  if (args->flags & RLX_F_SHARD) {  // cost-balanced block `serial_begin` of `serial_end` blocks
     const int64_t r = args->serial_begin, w = args->serial_end;
     if (w < 1 || r < 0 || r >= w) return fail(h, RLX_ERR_ARG, "bad shard index / count");
-    const int64_t q = hv.n_total / w, rem = hv.n_total % w;
-    b = r * q + (r < rem ? r : rem);
-    e = b + q + (r < rem ? 1 : 0);
+    shard_bounds(h->hp, r, w, b, e);
   }
   out->shard_begin = b;
   out->shard_end = e;
@@ -227,7 +250,7 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   // ---- upload plan (skipped when re-scoring the resident plan)
   size_t nb = h->hp.blob.buf.size();
   CK(cudaEventRecord(h->e2, h->stream));
-  if (reuse) {
+  if (h->plan_on_device) {
     nb = 0;
   } else if (nb > h->pin_cap) {
     if (h->h_pin) cudaFreeHost(h->h_pin);
@@ -240,8 +263,11 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
     CK(cudaMalloc(&h->d_blob, h->blob_cap));
   }
   if (nb) {
+    // the previous decision's kernel may still read d_blob / h_pin on this stream
+    CK(cudaStreamSynchronize(h->stream));
     memcpy(h->h_pin, h->hp.blob.buf.data(), nb);
     CK(cudaMemcpyAsync(h->d_blob, h->h_pin, nb, cudaMemcpyHostToDevice, h->stream));
+    h->plan_on_device = true;
   }
   out->h2d_bytes = (int64_t)nb;
   DevPlan dp;
@@ -259,7 +285,7 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   clip(hv.n_mux + hv.n_merge, hv.n_total, wd.c0, wd.nc);
   wd.shard0 = b;
   wd.counter = h->d_counter;
-  wd.err = h->d_err;
+  wd.err_key = h->d_errkey;
   if (args->keys_out) {
     size_t need = sizeof(double) * 2 * (size_t)(e - b);
     if (need > h->keys_cap) {
@@ -270,11 +296,9 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
     wd.keys_out = h->d_keys;
   }
   CK(cudaMemsetAsync(h->d_counter, 0, 8, h->stream));
-  CK(cudaMemsetAsync(h->d_err, 0, 32, h->stream));
-  CK(cudaMemsetAsync(h->d_dbg, 0, 16 * sizeof(double), h->stream));
-  wd.dbg = h->d_dbg;
-  wd.dbg_flag = h->d_err + 4;
+  CK(cudaMemsetAsync(h->d_errkey, 0xFF, 8, h->stream));
   int n_slices = 0;
+  std::lock_guard<std::mutex> lock(g_device_lock[h->device & 63]);
   CK(cudaEventRecord(h->e0, h->stream));
   rc = launch_score(dp, wd, (SliceOut*)h->d_outs, kMaxSlices, h->sm_count, h->stream, &n_slices, h->threads_hint);
   if (rc)
@@ -286,29 +310,18 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   if (args->dev_key_out)
     CK(cudaMemcpyAsync(args->dev_key_out, h->d_res, 32, cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(h->h_res, h->d_res, 64, cudaMemcpyDeviceToHost, h->stream));
-  int herr = 0;
-  CK(cudaMemcpyAsync(&h->h_res[8], h->d_err, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(&h->h_res[8], h->d_errkey, 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  herr = (int)(h->h_res[8] & 0xffffffffu);
+  const unsigned long long ek = h->h_res[8];
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->e0, h->e1);
   out->kernel_ms = ms;
   cudaEventElapsedTime(&ms, h->e2, h->e1);
   out->device_ms = ms;
-  out->d2h_bytes = 68;
-  if (herr) {
-    if (herr == RLX_ERR_SCHEDULING) {
-      cudaMemcpy(h->h_dbg, h->d_dbg, sizeof h->h_dbg, cudaMemcpyDeviceToHost);
-      char buf[400];
-      snprintf(buf, sizeof buf,
-               "window estimate did not converge (serial %.0f variant %.0f now %.17g done %.0f/%.0f tw_run %.0f "
-               "act %.0f/%.0f mt %.0f)",
-               h->h_dbg[1], h->h_dbg[2], h->h_dbg[3], h->h_dbg[4], h->h_dbg[5], h->h_dbg[6], h->h_dbg[10],
-               h->h_dbg[11], h->h_dbg[12]);
-      return fail(h, herr, buf);
-    }
-    if (herr == RLX_ERR_KEY) return fail(h, herr, "slowdown table or latency model has no entry for a queried pair");
-    return fail(h, herr, "device error");
+  out->d2h_bytes = 72;
+  if (ek != ~0ull) {  // the lowest failing serial of the shard: the candidate the reference raises on
+    out->serial = (int64_t)(ek >> 8);
+    return device_error(h, (int)(ek & 0xff));
   }
   unsigned long long* r = h->h_res;
   out->key.cost_bits = r[0];
@@ -333,6 +346,120 @@ int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, 
   if (args->keys_out)
     CK(cudaMemcpy(args->keys_out, h->d_keys, sizeof(double) * 2 * (size_t)(e - b), cudaMemcpyDeviceToHost));
   return RLX_OK;
+}
+
+int rlx_decide(void* handle, const RlxStateDesc* sd, const RlxDecideArgs* args, RlxDecision* out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !args || !out) return RLX_ERR_ARG;
+  return decide_impl(h, sd, args, out);
+}
+
+int rlx_drive(void* handle, void* state, const RlxDriveArgs* args, RlxStep* steps, int64_t* n_steps,
+              int64_t* n_decisions) {
+  Handle* h = (Handle*)handle;
+  ExecSoA* s = (ExecSoA*)state;
+  if (!h || !s || !args || !n_steps || !n_decisions || (args->max_steps > 0 && !steps)) return RLX_ERR_ARG;
+  *n_steps = 0;
+  *n_decisions = 0;
+  RlxDecideArgs da;
+  memset(&da, 0, sizeof da);
+  da.window = args->window;
+  da.max_merge = args->max_merge;
+  da.serial_begin = 0;
+  da.serial_end = -1;
+  const RlxInstanceDesc& in = h->inst;
+  auto alive_done = [&]() { return s->n_done == (int)s->order.size(); };
+  while (!alive_done()) {
+    for (;;) {  // decisions at this instant (scheduler.py:938-944)
+      if (args->max_decisions > 0 && *n_decisions >= args->max_decisions) return RLX_OK;
+      auto t0 = std::chrono::steady_clock::now();
+      RlxStateDesc sd;
+      s->snapshot(&sd);
+      RlxDecision d;
+      int rc = decide_impl(h, &sd, &da, &d);
+      if (rc) return rc;
+      if (d.n_candidates == 0) break;
+      (*n_decisions)++;
+      // winner (snapshot indices) -> state indices + LUT rates
+      RlxApply ap;
+      memset(&ap, 0, sizeof ap);
+      RlxAction act = d.action;
+      ap.cls = act.cls;
+      auto sidx = [&](int i) { return s->order[i]; };
+      auto lut = [&](int k, int partner, int alloc) {
+        return in.lut[(k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc];
+      };
+      if (act.cls == RLX_CLASS_MERGE) {
+        ap.n_members = act.n_members;
+        for (int i = 0; i < act.n_members; i++) ap.members[i] = act.members[i] = sidx(act.members[i]);
+        ap.target_worker = act.target_worker;
+      } else if (act.cls == RLX_CLASS_EXCLUSIVE) {
+        ap.node_a = act.node_a = sidx(act.node_a);
+        ap.rate_a = lut(s->nodes[ap.node_a].kind, -1, 0);
+        ap.sm_a = in.alloc_sm[0];
+        ap.mem_a = in.alloc_mem[0];
+      } else {
+        ap.node_a = act.node_a = sidx(act.node_a);
+        ap.node_b = act.node_b = sidx(act.node_b);
+        const int ka = s->nodes[ap.node_a].kind, kb = s->nodes[ap.node_b].kind;
+        ap.rate_a = lut(ka, kb, act.alloc);
+        ap.rate_b = lut(kb, ka, act.alloc + 12);
+        ap.sm_a = in.alloc_sm[act.alloc];
+        ap.mem_a = in.alloc_mem[act.alloc];
+        ap.sm_b = in.alloc_sm[act.alloc + 12];
+        ap.mem_b = in.alloc_mem[act.alloc + 12];
+      }
+      const double start = s->now;
+      rc = s->apply(&ap);
+      if (rc) return fail(h, rc, s->err);
+      if (*n_steps >= args->max_steps) return fail(h, RLX_ERR_LIMIT, "rlx_drive: steps array is full");
+      RlxStep& st = steps[(*n_steps)++];
+      memset(&st, 0, sizeof st);
+      st.start = start;
+      st.action = act;
+      st.cost = d.cost;
+      st.finish = d.finish;
+      st.priority = d.priority;
+      st.serial = d.serial;
+      st.n_candidates = d.n_candidates;
+      st.kernel_ms = d.kernel_ms;
+      st.decision_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (alive_done()) break;
+    if (s->run_order.empty() && s->tw_order.empty())
+      return fail(h, RLX_ERR_SCHEDULING, "lookahead: stalled with no running work");  // :948
+    int rc = s->advance(false, 0.0);
+    if (rc) return fail(h, rc, s->err);
+  }
+  return RLX_OK;
+}
+
+int rlx_plan_info(const RlxInstanceDesc* in, const RlxStateDesc* sd, int32_t window, int32_t max_merge,
+                  RlxPlanInfo* out, char* err, int32_t err_len) {
+  if (!in || !sd || !out) return RLX_ERR_ARG;
+  memset(out, 0, sizeof *out);
+  HostPlan hp;
+  std::string e;
+  int rc = window < 1 ? RLX_ERR_VALUE : build_plan(in, sd, window, max_merge, hp, e);
+  if (window < 1) e = "window must be >= 1";
+  if (!rc) {
+    const DevPlan& d = hp.dp;
+    out->n_candidates = d.n_total;
+    out->n_multiplex = d.n_mux;
+    out->n_merge = d.n_merge;
+    out->n_exclusive = d.n_excl;
+    out->window_nodes = d.NWIN;
+    out->local_nodes = d.NL;
+    out->max_worker_order = d.max_ord;
+    out->hot_bytes = (int32_t)hp.lay.hot_end;
+    out->blob_bytes = (int64_t)hp.blob.buf.size();
+    rc = check_capacity(hp, e);
+  }
+  if (err && err_len > 0) {
+    strncpy(err, e.c_str(), err_len - 1);
+    err[err_len - 1] = 0;
+  }
+  return rc;
 }
 
 int rlx_set_stream(void* handle, void* stream) {
@@ -365,11 +492,10 @@ void rlx_close(void* handle) {
   if (h->h_pin) cudaFreeHost(h->h_pin);
   if (h->d_outs) cudaFree(h->d_outs);
   if (h->d_counter) cudaFree(h->d_counter);
-  if (h->d_err) cudaFree(h->d_err);
+  if (h->d_errkey) cudaFree(h->d_errkey);
   if (h->d_res) cudaFree(h->d_res);
   if (h->h_res) cudaFreeHost(h->h_res);
   if (h->d_keys) cudaFree(h->d_keys);
-  if (h->d_dbg) cudaFree(h->d_dbg);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
   if (h->e2) cudaEventDestroy(h->e2);

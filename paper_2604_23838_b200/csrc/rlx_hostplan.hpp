@@ -50,6 +50,11 @@ struct HostPlan {
 int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, int max_merge, HostPlan& hp,
                std::string& err);
 void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d);
+void shard_bounds(const HostPlan& hp, int64_t r, int64_t w, int64_t& b, int64_t& e);
+int check_capacity(const HostPlan& hp, std::string& err);
+
+void choose_shape(int W, int& G, int& WPL);
+size_t plan_slice_bytes(const DevPlan& P, int G, int WPL);  // one group's slice
 
 // rlx_kernels.cu
 int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, int sm_count, cudaStream_t st,

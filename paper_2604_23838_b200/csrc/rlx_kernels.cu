@@ -98,6 +98,20 @@ RLX_HD unsigned long long at_add64(unsigned long long* p, unsigned long long v) 
   return o;
 #endif
 }
+RLX_HD void at_min64(unsigned long long* p, unsigned long long v) {
+#ifdef __CUDA_ARCH__
+  atomicMin(p, v);
+#else
+  if (v < *p) *p = v;
+#endif
+}
+template <int G>
+RLX_HD int gmax(unsigned m, int x) {
+#ifdef __CUDA_ARCH__
+  if (G > 1) return __reduce_max_sync(m, x);
+#endif
+  return x;
+}
 RLX_HD int at_cas(int* p, int c, int v) {
 #ifdef __CUDA_ARCH__
   return atomicCAS(p, c, v);
@@ -159,6 +173,16 @@ RLX_HD double defmem(int k) {
   return k == 0 ? 0.5 : k == 1 ? 0.55 : k == 2 ? 0.4 : k == 3 ? 0.3 : k == 4 ? 0.5 : k == 5 ? 0.6 : 0.05;
 }
 
+// Candidate error codes (per lane / group): RLX_ERR_SCHEDULING for the
+// window guard, kErrLatBase + bucket for a missing latency bucket
+// (merged_estimate :197), key_err(kind, partner) for a missing slowdown row
+// (slowdown.py:143-147). The kernel keeps the LOWEST failing serial
+// (err_key = serial << 8 | code, atomicMin), the one the reference's serial
+// scan raises on.
+constexpr int kErrLatBase = 8;
+constexpr int kErrKeyBase = 16;
+RLX_HD int key_err(int k, int partner) { return kErrKeyBase + k * RLX_NPARTNER + partner + 1; }
+
 RLX_HD unsigned long long dbits(double x) {
   unsigned long long b;
   memcpy(&b, &x, 8);
@@ -201,6 +225,7 @@ struct GroupCand {
   int phase, y, oo, ai, mj, v;  // pass iterator
   int fa, fb, falloc;     // follow-up action of the current pass
   int twq_n, tw_run;
+  int cerr;  // error of the current candidate (first failure), 0 if none
   int dsum;  // window completions of the running pass (plans without tool waits)
   uint16_t m[kMaxMembers];
 };
@@ -244,14 +269,11 @@ struct Lane {
   Bits pm;    // bit 2j+s: has a non-zero prefix (value in the slice)
   Bits pf;    // bit 2j+s: still has a multiplex partner
   double tl;  // this lane's next-event candidate time
-  int o, mt, ins, err;
+  int o, mt, ins, err;  // err: 0, RLX_ERR_SCHEDULING or key_err(...) (first failure of this candidate)
   // pass registers
   double now, last;
   int done_cnt, guard;
   bool any_done;
-  // guard-failure report
-  double* dbg = nullptr;
-  int* dbg_flag = nullptr;
 
   RLX_HD Lane(uint32_t gb, int ln, unsigned m) : gbase(gb), lane(ln), gm(m) {
     err = 0;
@@ -290,7 +312,7 @@ struct Lane {
 
   RLX_HD double L3(int k, int partner, int alloc) {
     double v = lutv((k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc);
-    if (isnan(v)) err = RLX_ERR_KEY;
+    if (isnan(v) && err < kErrKeyBase) err = key_err(k, partner);
     return v;
   }
   RLX_HD int node_at(int w, int p) const {
@@ -529,8 +551,9 @@ struct Lane {
               const uint8_t* po = arr<uint8_t>(PLAN.o_pos) + PLAN.NL;  // name-order positions
               const int ent =
                   arr<uint8_t>(PLAN.o_ptab)[arr<uint32_t>(PLAN.o_pt_off)[w] + po[x] * cnt + po[y]];
-              if (ent == 0x60) {
-                err = RLX_ERR_KEY;
+              if (ent >= 0x60 && ent < 0x80) {
+                if (err < kErrKeyBase)  // the first LUT lookup of _best_pair_action that misses
+                  err = (ent & 1) ? key_err(hkind(y), hkind(x)) : key_err(hkind(x), hkind(y));
               } else if (ent) {
                 paired = true;
                 al = ent & 31;
@@ -645,16 +668,7 @@ struct Lane {
     const double t = gmin<G>(gm, tl);
     if (t == INFINITY && twr == 0) return false;
     if (++guard > 10000) {  // scheduler.py:866-867
-      err = RLX_ERR_SCHEDULING;
-      if (dbg && lane == 0 && at_cas(dbg_flag, 0, 1) == 0) {
-        dbg[1] = (double)serial;
-        dbg[2] = variant;
-        dbg[3] = now;
-        dbg[4] = done_cnt;
-        dbg[5] = nwin;
-        dbg[6] = twr;
-        dbg[12] = mt;
-      }
+      if (!err) err = RLX_ERR_SCHEDULING;
       return false;
     }
     double dt = t - now;
@@ -727,7 +741,7 @@ struct Lane {
 // Merged node of a Merge candidate (_apply_merge :517-581, merged_estimate
 // :185-199, migration_cost :174-182) and its insertion point in both worker
 // orders (ids compare as Python str). Group leader only.
-RLX_HD void setup_merge(const Cand& c, GroupCand* sc, int* gerr) {
+RLX_HD void setup_merge(const Cand& c, GroupCand* sc) {
   long long tokens = 0, active = 0;
   double dmax = 0.0, mmax = 0.0, sfx = 0.0;
   const int p = PLAN.pipe[c.m[0]];
@@ -748,7 +762,7 @@ RLX_HD void setup_merge(const Cand& c, GroupCand* sc, int* gerr) {
   } else {
     const int bk = active >= 1024 ? 2 : (active >= 128 ? 1 : 0);
     kd = bk == 0 ? RLX_KIND_DECODE_SMALL : (bk == 1 ? RLX_KIND_DECODE_MEDIUM : RLX_KIND_DECODE_LARGE);
-    if (!PLAN.latency_ok[p * 3 + bk]) at_cas(gerr, 0, RLX_ERR_KEY);
+    if (!PLAN.latency_ok[p * 3 + bk]) sc->cerr = kErrLatBase + bk;  // latency_model[bucket] KeyError
     du = ((double)tokens * PLAN.latency[p * 3 + bk]) / (double)active;
   }
   double pre = 0.0;
@@ -897,14 +911,13 @@ RLX_HD bool next_action(GroupCand* g) {
 template <int G, int WPL>
 RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm, SliceOut* out) {
   Lane<G, WPL> S(gbase, lane, gm);
-  S.dbg = wd.dbg;
-  S.dbg_flag = wd.dbg_flag;
   GroupCand* g = S.gc();
   if (lane == 0) {
     g->b0 = g->b1 = g->b2 = ~0ull;
     g->passes = g->ncand = g->events = 0;
     g->bytes = 0.0;
     g->cls = -1;
+    g->cerr = 0;
   }
   gsync<G>(gm);
   const int64_t total = wd.na + wd.nb + wd.nc;
@@ -921,43 +934,56 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
       gsync<G>(gm);
       if (g->cls >= 0) {
         const double x = S.any_done ? S.last : S.now;
+        const int e = gmax<G>(gm, S.err);  // the pass failed on some lane: the candidate raises
         gsync<G>(gm);
         if (lane == 0) {
           g->events += (unsigned long long)S.guard;
-          if (x < g->cost) g->cost = x;
-          more = next_action(g);
+          if (e > g->cerr) g->cerr = e;
+          if (!g->cerr) {
+            if (x < g->cost) g->cost = x;
+            more = next_action(g);
+          }
         }
         more = gbcast<G>(gm, more ? 1 : 0) != 0;
         gsync<G>(gm);
       }
       if (!more) {
         if (g->cls >= 0 && lane == 0) {  // finished candidate: key (cost, finish, priority, serial)
-          if (S.err) at_cas(wd.err, 0, S.err);
-          g->ncand++;
-          const unsigned long long k0 = dbits(g->cost), k1 = dbits(g->fin);
-          const unsigned long long k2 = ((unsigned long long)g->cls << 61) | (unsigned long long)g->serial;
-          if (key_less(k0, k1, k2, g->b0, g->b1, g->b2)) {
-            g->b0 = k0;
-            g->b1 = k1;
-            g->b2 = k2;
-          }
-          if (wd.keys_out) {
-            wd.keys_out[2 * (g->serial - wd.shard0)] = g->cost;
-            wd.keys_out[2 * (g->serial - wd.shard0) + 1] = g->fin;
+          if (g->cerr) {
+            // the reference raises on the first failing candidate of its serial scan
+            at_min64(wd.err_key, ((unsigned long long)g->serial << 8) | (unsigned long long)g->cerr);
+          } else {
+            g->ncand++;
+            const unsigned long long k0 = dbits(g->cost), k1 = dbits(g->fin);
+            const unsigned long long k2 = ((unsigned long long)g->cls << 61) | (unsigned long long)g->serial;
+            if (key_less(k0, k1, k2, g->b0, g->b1, g->b2)) {
+              g->b0 = k0;
+              g->b1 = k1;
+              g->b2 = k2;
+            }
+            if (wd.keys_out) {
+              wd.keys_out[2 * (g->serial - wd.shard0)] = g->cost;
+              wd.keys_out[2 * (g->serial - wd.shard0) + 1] = g->fin;
+            }
           }
         }
-        // ---- next candidate (heaviest class first)
-        long long idx = 0;
+        S.err = 0;
+        // ---- next candidate (heaviest class first); once some candidate
+        // failed, only lower serials can still change the outcome
+        long long idx = 0, serial = 0;
         if (lane == 0) {
-          idx = (long long)at_add64(wd.counter, 1ull);
-          if (*(volatile int*)wd.err) idx = total;
+          for (;;) {
+            idx = (long long)at_add64(wd.counter, 1ull);
+            if (idx >= total) break;
+            serial = idx < wd.na ? wd.a0 + idx
+                                 : (idx < wd.na + wd.nb ? wd.b0 + (idx - wd.na) : wd.c0 + (idx - wd.na - wd.nb));
+            if ((unsigned long long)serial <= (*(volatile unsigned long long*)wd.err_key >> 8)) break;
+          }
         }
         idx = gbcast<G>(gm, idx);
         if (idx >= total) break;
         gsync<G>(gm);  // every lane has read the previous candidate's fields
         if (lane == 0) {
-          const int64_t serial = idx < wd.na ? wd.a0 + idx
-                                             : (idx < wd.na + wd.nb ? wd.b0 + (idx - wd.na) : wd.c0 + (idx - wd.na - wd.nb));
           Cand c;
           decode_serial(PLAN, serial, c);
           g->serial = serial;
@@ -965,8 +991,9 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
           g->cost = INFINITY;
           g->v = 0;
           g->phase = 0;
+          g->cerr = 0;
           if (c.cls == 1) {
-            setup_merge(c, g, wd.err);
+            setup_merge(c, g);
             g->fin = (PLAN.now + g->pre) + g->dur;
             g->nwin = PLAN.NWIN - c.k + 1;
             g->rm = PLAN.mask0[1 * PLAN.W + g->t];
@@ -1003,6 +1030,7 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
         }
         gsync<G>(gm);
       }
+      if (g->cerr) continue;  // merged_estimate raised: no pass runs (boundary records the error)
       // ---- start the pass
       const bool is_merge = g->cls == 1;
       variant = g->v;
@@ -1029,7 +1057,6 @@ RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm
     }
     active = S.step(pair, nwin, g->serial, variant);
   }
-  if (S.err) at_cas(wd.err, 0, S.err);
   gsync<G>(gm);
   if (lane == 0) {
     out->k0 = g->b0;
@@ -1177,6 +1204,12 @@ void choose_shape(int W, int& G, int& WPL) {
   while (G * WPL < W) G *= 2;
 }
 
+size_t plan_slice_bytes(const DevPlan& P, int G, int WPL) {
+  DevPlan P2 = P;
+  group_layout(P2, G, WPL);
+  return P2.g_bytes;
+}
+
 static KernelFn pick(int G, int WPL) {
   if (WPL == 1) {
     switch (G) {
@@ -1227,7 +1260,7 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
   const size_t gb = P2.g_bytes;
   wd.slice_bytes = (int)gb;
   const size_t hot = P.hot_bytes;
-  const size_t cap = 227 * 1024 - 64;
+  const size_t cap = kSmemCap;
   if (hot + gb > cap) return RLX_ERR_LIMIT;
   int threads = threads_hint > 0 && threads_hint <= threads_for(WPL) ? threads_hint : threads_for(WPL);
   while (threads > G && hot + (size_t)(threads / G) * gb > cap) threads /= 2;

@@ -297,15 +297,17 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   // of window compute nodes of different pipelines on the same worker. It is
   // decision-invariant, so pairing passes look it up instead of searching the
   // 24-point orientation x alpha x mem grid. Entry: 0 = no feasible pair,
-  // else 0x80 | (second-is-x) << 6 | alloc; 0x40|0x20 flags a missing LUT row.
+  // else 0x80 | (second-is-x) << 6 | alloc; 0x60 | r flags a missing LUT row
+  // (r = 0: the first missing lookup is (kind x, kind y), r = 1: (kind y, kind x)).
   std::vector<uint32_t> pt_off(W + 1, 0);
   std::vector<uint8_t> ptab;
   {
     const double hr = in->headroom;
     static const double MGP[4] = {0.20, 0.40, 0.60, 0.80};
-    auto L3 = [&](int k, int partner, int alloc, bool& bad) {
+    // bad: 0 none, 1 first missing lookup is (kind x, kind y), 2 it is (kind y, kind x)
+    auto L3 = [&](int k, int partner, int alloc, int& bad, int code) {
       double v = in->lut[(k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc];
-      if (std::isnan(v)) bad = true;
+      if (std::isnan(v) && !bad) bad = code;
       return v;
     };
     auto rerated = [](double da, double sa, double db, double sb) {
@@ -325,7 +327,7 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
           if (!(mem[a] + mem[b] <= 1.0 - hr + 1e-12)) continue;
           double best = INFINITY;
           int ent = 0;
-          bool bad = false;
+          int bad = 0;
           for (int oo = 0; oo < 2; oo++) {
             const int f = oo ? b : a, sc2 = oo ? a : b;
             const double ms = mem[sc2];
@@ -333,15 +335,17 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
               for (int mj = 0; mj < 4; mj++) {
                 if (MGP[mj] + ms > 1.0 - hr + kEps) continue;
                 const int al = 1 + ai * 4 + mj;
-                const double e = rerated(dur[f], L3(kind[f], kind[sc2], al, bad), dur[sc2],
-                                         L3(kind[sc2], kind[f], al + 12, bad));
+                // argument order of _rerated_pair_end(...) (:816-821): first's factor is looked up first
+                const double sf = L3(kind[f], kind[sc2], al, bad, oo ? 2 : 1);
+                const double ss = L3(kind[sc2], kind[f], al + 12, bad, oo ? 1 : 2);
+                const double e = rerated(dur[f], sf, dur[sc2], ss);
                 if (e < best - kEps) {
                   best = e;
                   ent = 0x80 | (oo << 6) | al;
                 }
               }
           }
-          ptab[pt_off[w] + (size_t)px * cnt + py] = bad ? 0x60 : (uint8_t)ent;
+          ptab[pt_off[w] + (size_t)px * cnt + py] = bad ? (uint8_t)(0x60 | (bad - 1)) : (uint8_t)ent;
         }
     }
     pt_off[W] = (uint32_t)ptab.size();
@@ -584,6 +588,29 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.frags = B.putv(hp.frags);
   L.combos = B.putv(hp.combos);
   L.binom = B.putv(hp.binom);
+  return RLX_OK;
+}
+
+// Serial block `r` of `w` (RLX_F_SHARD): contiguous, sizes differ by <= 1.
+void shard_bounds(const HostPlan& hp, int64_t r, int64_t w, int64_t& b, int64_t& e) {
+  const int64_t n = hp.dp.n_total, q = n / w, rem = n % w;
+  b = r * q + (r < rem ? r : rem);
+  e = b + q + (r < rem ? 1 : 0);
+}
+
+// The device path's capacity checks that depend only on the plan: a kernel
+// shape for W workers and the shared-memory footprint of the hot region.
+int check_capacity(const HostPlan& hp, std::string& err) {
+  int G, WPL;
+  choose_shape(hp.dp.W, G, WPL);
+  if (G > 32 || G * WPL < hp.dp.W) {
+    err = "more than 128 workers";
+    return RLX_ERR_LIMIT;
+  }
+  if (hp.lay.hot_end + plan_slice_bytes(hp.dp, G, WPL) > kSmemCap) {
+    err = "the plan does not fit in shared memory";
+    return RLX_ERR_LIMIT;
+  }
   return RLX_OK;
 }
 

@@ -32,6 +32,7 @@ constexpr int kMaxMembers = 64;    // merge members
 constexpr int kMaxFrags = 128;     // fragments per pipeline for unranking
 constexpr int kBinomK = 65;        // binomial table columns
 constexpr double kEps = 1e-9;      // scheduler.py:43
+constexpr unsigned kSmemCap = 227 * 1024 - 64;  // dynamic shared memory per CTA (sm_100)
 
 // node flags
 constexpr uint8_t F_TW = 1;        // ToolWait kind
@@ -152,10 +153,8 @@ struct WorkDesc {
   int64_t shard0;   // keys_out index base
   double* keys_out; // device, optional
   unsigned long long* counter;
-  int* err;
+  unsigned long long* err_key;  // lowest failing candidate: serial << 8 | error code (~0: none)
   int slice_bytes;  // shared-memory bytes per group (DevPlan::g_bytes)
-  double* dbg;      // device, 16 doubles: first guard failure (serial, variant, now, counters)
-  int* dbg_flag;    // device: 0 until the first failure claims dbg
 };
 
 // Decoded candidate.

@@ -7,9 +7,10 @@ rlmux/scheduler.py:671-675) and their complements (slowdown.py:169-175) —
 for all (kind, partner) pairs, evaluated here with the reference's own
 bilinear op order so the device only does table lookups.
 
-`StateEncoding` is a snapshot of `HostState` at a decision point. Node
-arrays are cached per structural revision (merges change the graph), so an
-undisturbed decision only refreshes the dynamic vectors.
+`GraphEncoding` is the static sub-stage graph the native execution state
+(`state.State`, csrc/rlx_state.cpp) is created from; the per-decision
+state the device consumes is a view of that native state, not a Python
+re-encode.
 """
 
 from __future__ import annotations
@@ -124,78 +125,44 @@ class InstanceEncoding:
         self.desc = d
 
 
-class StateEncoding:
-    """Flat snapshot of a HostState (scheduler.py:339-366 fields)."""
+class GraphEncoding:
+    """The static sub-stage graph of an instance (include/rlx.h
+    RlxGraphDesc): every graph's nodes in Instance.graphs order, then node
+    insertion order — the reference ExecState's dict order
+    (scheduler.py:348-356)."""
 
-    def __init__(self, enc: InstanceEncoding):
-        self.enc = enc
-        self._rev = None
-
-    def _structure(self, st):
-        enc = self.enc
-        order = list(st.nodes)
-        self.order = order
-        self.index = {nid: i for i, nid in enumerate(order)}
-        n = len(order)
-        nodes = [st.nodes[k] for k in order]
-        self.pipe = np.array([enc.pipe_index[x.pipeline_id] for x in nodes], dtype=np.int32)
-        self.worker = np.array([enc.worker_index[x.worker_id] for x in nodes], dtype=np.int32)
-        self.kind = np.array([KIND_CODE[x.kind] for x in nodes], dtype=np.int32)
-        self.duration = np.array([x.duration for x in nodes], dtype=np.float64)
-        self.mem = np.array([x.mem_fraction for x in nodes], dtype=np.float64)
-        self.remaining = np.array([x.remaining_decode_tokens for x in nodes], dtype=np.int64)
-        self.active = np.array([x.active_requests for x in nodes], dtype=np.int64)
-        self.context = np.array([x.context_tokens for x in nodes], dtype=np.int64)
+    def __init__(self, instance, enc: "InstanceEncoding"):
+        nodes = [n for g in instance.graphs for n in g.nodes.values()]
+        self.ids = [n.id for n in nodes]
+        self.index = {nid: i for i, nid in enumerate(self.ids)}
+        self.pipe = np.array([enc.pipe_index[n.pipeline_id] for n in nodes], dtype=np.int32)
+        self.worker = np.array([enc.worker_index[n.worker_id] for n in nodes], dtype=np.int32)
+        self.kind = np.array([KIND_CODE[n.kind] for n in nodes], dtype=np.int32)
+        self.duration = np.array([n.duration for n in nodes], dtype=np.float64)
+        self.mem = np.array([n.mem_fraction for n in nodes], dtype=np.float64)
+        self.remaining = np.array([n.remaining_decode_tokens for n in nodes], dtype=np.int64)
+        self.active = np.array([n.active_requests for n in nodes], dtype=np.int64)
+        self.context = np.array([n.context_tokens for n in nodes], dtype=np.int64)
+        self.token_total = np.array([n.token_total for n in nodes], dtype=np.int64)
+        self.span_lo = np.array([n.step_span[0] for n in nodes], dtype=np.int64)
+        self.span_hi = np.array([n.step_span[1] for n in nodes], dtype=np.int64)
         blob = bytearray()
-        offs = np.zeros(n, dtype=np.int32)
-        for i, k in enumerate(order):
+        offs = np.zeros(len(nodes), dtype=np.int32)
+        for i, nid in enumerate(self.ids):
             offs[i] = len(blob)
-            blob += k.encode("utf-8") + b"\0"
+            blob += nid.encode("utf-8") + b"\0"
         self._ids = bytes(blob)
         self.id_off = offs
         src, dst = [], []
-        idx = self.index
-        for k in order:
-            i = idx[k]
-            for s in st.succs[k]:
-                src.append(i)
-                dst.append(idx[s])
+        for g in instance.graphs:
+            for a, b in g.edges:
+                src.append(self.index[a])
+                dst.append(self.index[b])
         self.edge_src = np.array(src, dtype=np.int32)
         self.edge_dst = np.array(dst, dtype=np.int32)
-        self._rev = (id(st), st.revision)
-
-    def encode(self, st):
-        if self._rev != (id(st), st.revision):
-            self._structure(st)
-        enc = self.enc
-        idx = self.index
-        n = len(self.order)
-        self.completed = np.zeros(n, dtype=np.uint8)
-        for k in st.completed:
-            self.completed[idx[k]] = 1
-        self.merge_prefix = np.zeros(n, dtype=np.float64)
-        for k, v in st.merge_prefix.items():
-            i = idx.get(k)  # a merged node merged again leaves a dead entry (reference quirk)
-            if i is not None:
-                self.merge_prefix[i] = v
-        run = list(st.running.items())
-        self.run_node = np.array([idx[k] for k, _ in run], dtype=np.int32)
-        self.run_partner = np.array([idx[m.partner_id] if m.partner_id is not None else -1 for _, m in run],
-                                    dtype=np.int32)
-        self.run_rate = np.array([m.rate for _, m in run], dtype=np.float64)
-        self.run_prefix = np.array([m.prefix_left for _, m in run], dtype=np.float64)
-        self.run_work = np.array([m.work_left for _, m in run], dtype=np.float64)
-        tws = list(st.toolwaits.items())
-        self.tw_node = np.array([idx[k] for k, _ in tws], dtype=np.int32)
-        self.tw_end = np.array([t for _, t in tws], dtype=np.float64)
-        grants = list(st.last_mem_grant.items())
-        self.grant_worker = np.array([enc.worker_index[w] for (w, _), _ in grants], dtype=np.int32)
-        self.grant_pipe = np.array([enc.pipe_index[p] for (_, p), _ in grants], dtype=np.int32)
-        self.grant_mem = np.array([m for _, m in grants], dtype=np.float64)
-        d = abi.RlxStateDesc()
-        d.now = st.now
-        d.n_nodes = n
-        d.n_edges = len(self.edge_src)
+        d = abi.RlxGraphDesc()
+        d.n_nodes = len(nodes)
+        d.n_edges = len(src)
         d.pipe = _ptr(self.pipe, C.c_int32)
         d.worker = _ptr(self.worker, C.c_int32)
         d.kind = _ptr(self.kind, C.c_int32)
@@ -204,42 +171,28 @@ class StateEncoding:
         d.remaining = _ptr(self.remaining, C.c_int64)
         d.active = _ptr(self.active, C.c_int64)
         d.context = _ptr(self.context, C.c_int64)
-        d.completed = _ptr(self.completed, C.c_uint8)
-        d.merge_prefix = _ptr(self.merge_prefix, C.c_double)
+        d.token_total = _ptr(self.token_total, C.c_int64)
+        d.span_lo = _ptr(self.span_lo, C.c_int64)
+        d.span_hi = _ptr(self.span_hi, C.c_int64)
         d.ids = self._ids
         d.id_off = _ptr(self.id_off, C.c_int32)
         d.edge_src = _ptr(self.edge_src, C.c_int32)
         d.edge_dst = _ptr(self.edge_dst, C.c_int32)
-        d.n_running = len(run)
-        d.n_toolwaits = len(tws)
-        d.run_node = _ptr(self.run_node, C.c_int32)
-        d.run_partner = _ptr(self.run_partner, C.c_int32)
-        d.run_rate = _ptr(self.run_rate, C.c_double)
-        d.run_prefix = _ptr(self.run_prefix, C.c_double)
-        d.run_work = _ptr(self.run_work, C.c_double)
-        d.tw_node = _ptr(self.tw_node, C.c_int32)
-        d.tw_end = _ptr(self.tw_end, C.c_double)
-        d.n_grants = len(grants)
-        d.grant_worker = _ptr(self.grant_worker, C.c_int32)
-        d.grant_pipe = _ptr(self.grant_pipe, C.c_int32)
-        d.grant_mem = _ptr(self.grant_mem, C.c_double)
-        # the descriptor owns the arrays it points into, so it stays valid
-        # after a later encode() rebinds the attributes above
-        d._keep = (self.pipe, self.worker, self.kind, self.duration, self.mem, self.remaining, self.active,
-                   self.context, self.completed, self.merge_prefix, self._ids, self.id_off, self.edge_src,
-                   self.edge_dst, self.run_node, self.run_partner, self.run_rate, self.run_prefix, self.run_work,
-                   self.tw_node, self.tw_end, self.grant_worker, self.grant_pipe, self.grant_mem)
         self.desc = d
-        return d
 
-    def action_from_raw(self, a: abi.RlxAction):
-        """Decoded RlxAction -> Exclusive / Multiplex / Merge of this package."""
-        from .model import Exclusive, Merge, Multiplex
 
-        order = self.order
-        if a.cls == abi.CLASS_EXCLUSIVE:
-            return Exclusive(order[a.node_a])
-        if a.cls == abi.CLASS_MULTIPLEX:
-            return Multiplex(order[a.node_a], order[a.node_b], self.enc.allocs[a.alloc])
-        ids = tuple(order[a.members[i]] for i in range(a.n_members))
-        return Merge(ids, self.enc.workers[a.target_worker])
+def _knobs(instance) -> tuple:
+    return (instance.headroom, instance.realloc_penalty, instance.default_migration_cost, instance.merge_enabled,
+            id(instance.model), len(instance.graphs))
+
+
+def instance_encoding(instance) -> "InstanceEncoding":
+    """The instance's C-ABI encoding, built once per Instance object (and
+    rebuilt if its knobs are changed afterwards)."""
+    cached = instance.__dict__.get("_rlx_encoding")
+    if cached is not None and cached[0] == _knobs(instance):
+        return cached[1]
+    enc = InstanceEncoding(instance)
+    enc.graph = GraphEncoding(instance, enc)
+    instance.__dict__["_rlx_encoding"] = (_knobs(instance), enc)
+    return enc

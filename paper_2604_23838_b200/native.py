@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 from . import abi
-from .encode import InstanceEncoding, StateEncoding
+from .encode import instance_encoding
 from .model import SchedulingError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -26,7 +26,10 @@ class NativeUnavailable(RuntimeError):
     pass
 
 
-def load_library(path: str = LIB_PATH) -> C.CDLL:
+def load_library(path: str = LIB_PATH, require_device: bool = True) -> C.CDLL:
+    """The in-tree CUDA library. Loading needs no device (the native
+    execution state and the host planner run without one); scoring does
+    (`Evaluator` raises NativeUnavailable when rlx_open finds no GPU)."""
     global _lib
     if _lib is None:
         if not os.path.exists(path):
@@ -37,14 +40,44 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     return _lib
 
 
-def _raise(code: int, msg: str):
+class CapacityError(RuntimeError):
+    """The input exceeds a compiled limit of this build (RLX_ERR_LIMIT,
+    include/rlx.h); the reference itself has no such limit. INTEGRATION.md §4
+    lists them."""
+
+
+def _raise(code: int, msg: str, serial: int | None = None):
+    """Status code -> the reference's exception class. A failing candidate's
+    serial rides on the exception (`.serial`), the message is the
+    reference's text."""
     if code == abi.RLX_ERR_SCHEDULING:
-        raise SchedulingError(msg)
-    if code == abi.RLX_ERR_KEY:
-        raise KeyError(msg)
-    if code == abi.RLX_ERR_VALUE:
-        raise ValueError(msg)
-    raise RuntimeError(f"rlx status {code}: {msg}")
+        exc = SchedulingError(msg)
+    elif code == abi.RLX_ERR_KEY:
+        exc = KeyError(msg)
+    elif code == abi.RLX_ERR_VALUE:
+        exc = ValueError(msg)
+    elif code == abi.RLX_ERR_LIMIT:
+        exc = CapacityError(msg)
+    else:
+        exc = RuntimeError(f"rlx status {code}: {msg}")
+    exc.serial = serial
+    exc.code = code
+    raise exc
+
+
+def plan_info(state, window: int, max_merge: int | None = None) -> abi.RlxPlanInfo:
+    """Host-only planning of `state`'s decision (rlx_plan_info): candidate
+    counts and plan sizes, or the CapacityError the device path would
+    raise. Needs no GPU."""
+    lib = load_library(require_device=False)
+    out = abi.RlxPlanInfo()
+    err = C.create_string_buffer(512)
+    sd = state.snapshot()
+    rc = lib.rlx_plan_info(C.byref(state.enc.desc), C.byref(sd), int(window),
+                           0 if max_merge is None else int(max_merge), C.byref(out), err, 512)
+    if rc != 0:
+        _raise(rc, err.value.decode())
+    return out
 
 
 class Evaluator:
@@ -60,14 +93,15 @@ class Evaluator:
         self.device = device
         self.instance = None
         self.last = None
+        self.last_state = None
+        self.n_decisions = 0
         self.history = []  # per-decision RlxDecision copies (stats)
         self.record = False
         if instance is not None:
             self.bind(instance)
 
     def bind(self, instance) -> None:
-        self.enc = InstanceEncoding(instance)
-        self.senc = StateEncoding(self.enc)
+        self.enc = instance_encoding(instance)
         rc = self.lib.rlx_load_instance(self.handle, C.byref(self.enc.desc))
         if rc != 0:
             _raise(rc, self.error())
@@ -89,17 +123,14 @@ class Evaluator:
 
     def decide(self, state, window: int, max_merge: int | None = None, shard=None, want_keys=False,
                dev_key_ptr: int | None = None, part=None) -> abi.RlxDecision:
-        """Score every candidate of `state` on the GPU — or the serial shard
-        [b, e) (`shard`), or contiguous block r of w (`part=(r, w)`, sized by
-        the library from the candidate count, dist.shard_range)."""
-        n_all = self.count(state, window, max_merge) if (want_keys and shard is None) else None
-        # encode AFTER count(): every encode() replaces the arrays the previous
-        # descriptor points into
-        sd = self.senc.encode(state)
+        """Score every candidate of `state` (a `state.State`) on the GPU —
+        or the serial shard [b, e) (`shard`, e < 0: to the last candidate),
+        or cost-balanced part r of w (`part=(r, w)`, dist.py)."""
+        self._check_state(state)
         args = abi.RlxDecideArgs()
         args.window = int(window)
         args.max_merge = 0 if max_merge is None else int(max_merge)
-        args.serial_begin, args.serial_end = (0, -1) if shard is None else (int(shard[0]), int(shard[1]))
+        b, e = (0, -1) if shard is None else (int(shard[0]), int(shard[1]))
         if part is not None:
             if want_keys:
                 raise ValueError("want_keys needs an explicit shard")
@@ -107,21 +138,57 @@ class Evaluator:
             args.flags |= abi.RLX_F_SHARD
         keys = None
         if want_keys:
-            n = n_all if shard is None else shard[1] - shard[0]
-            keys = np.zeros((max(int(n), 1), 2), dtype=np.float64)
+            if e < 0 or b < 0:  # resolve "to the last candidate" before sizing the buffer
+                n = plan_info(state, window, max_merge).n_candidates
+                b = max(b, 0)
+                e = n if e < 0 else e
+            keys = np.zeros((max(e - b, 1), 2), dtype=np.float64)
             args.keys_out = keys.ctypes.data_as(C.POINTER(C.c_double))
+        if part is None:
+            args.serial_begin, args.serial_end = b, e
         args.dev_key_out = dev_key_ptr
+        sd = state.snapshot()
         out = abi.RlxDecision()
         rc = self.lib.rlx_decide(self.handle, C.byref(sd), C.byref(args), C.byref(out))
         if rc != 0:
-            _raise(rc, self.error())
+            _raise(rc, self.error(), out.serial if out.serial >= 0 else None)
         self.last = out
+        self.last_state = state
         if self.record:
             self.history.append(out)
         if want_keys:
-            nk = out.n_candidates if shard is None else min(shard[1], out.n_candidates) - shard[0]
+            nk = min(e, out.n_candidates) - b
             self.keys = keys[: max(int(nk), 0)]
         return out
+
+    def _check_state(self, state) -> None:
+        if state.instance is not self.instance and state.enc is not self.enc:
+            raise ValueError("the state belongs to a different instance than this Evaluator is bound to")
+
+    def schedule(self, state, window: int, max_merge: int | None = None, max_decisions: int | None = None):
+        """The whole decision loop (`_drive`, scheduler.py:925-950) behind
+        one C call (rlx_drive): plan -> score -> argmin -> apply the winner to
+        the native `state` -> advance, until done. Returns the RlxStep
+        records (applied actions, their keys and decision latencies);
+        `state.replay_steps` turns them into actions."""
+        self._check_state(state)
+        info = state.info()
+        cap = 2 * info.n_total + 8
+        steps = (abi.RlxStep * cap)()
+        args = abi.RlxDriveArgs()
+        args.window = int(window)
+        args.max_merge = 0 if max_merge is None else int(max_merge)
+        args.max_decisions = 0 if max_decisions is None else int(max_decisions)
+        args.max_steps = cap
+        n_steps = C.c_int64()
+        n_dec = C.c_int64()
+        rc = self.lib.rlx_drive(self.handle, state.handle, C.byref(args), steps, C.byref(n_steps), C.byref(n_dec))
+        done = list(steps[: n_steps.value])
+        self.n_decisions = n_dec.value
+        if rc != 0:
+            state.replay_steps(done)  # keep the id mirror in step with the native state
+            _raise(rc, self.error())
+        return done
 
     def rescore(self, window: int, shard=None, dev_key_ptr: int | None = None, part=None) -> abi.RlxDecision:
         """Re-run scoring + argmin on the plan already resident on the device
@@ -149,24 +216,16 @@ class Evaluator:
             _raise(rc, self.error())
 
     def count(self, state, window: int, max_merge: int | None = None) -> int:
-        """Candidate count of a state (planning only: an empty shard)."""
-        sd = self.senc.encode(state)
-        args = abi.RlxDecideArgs()
-        args.window = int(window)
-        args.max_merge = 0 if max_merge is None else int(max_merge)
-        args.serial_begin, args.serial_end = 0, 0
-        out = abi.RlxDecision()
-        rc = self.lib.rlx_decide(self.handle, C.byref(sd), C.byref(args), C.byref(out))
-        if rc != 0:
-            _raise(rc, self.error())
-        return out.n_candidates
+        """Candidate count of a state (host planning only)."""
+        return plan_info(state, window, max_merge).n_candidates
 
     def decode(self, serial: int):
+        """Serial of the last decided state -> its action."""
         a = abi.RlxAction()
         rc = self.lib.rlx_decode(self.handle, int(serial), C.byref(a))
         if rc != 0:
             _raise(rc, self.error())
-        return self.senc.action_from_raw(a)
+        return self.last_state.action_from_raw(a)
 
     def chooser(self, window: int, max_merge: int | None = None, log=None, group=None):
         """A `drive` chooser deciding on this GPU (or, with a process group,
@@ -180,7 +239,7 @@ class Evaluator:
             d = self.decide(state, window, max_merge)
             if d.n_candidates == 0:
                 return None
-            action = self.senc.action_from_raw(d.action)
+            action = state.action_from_raw(d.action)
             if log is not None:
                 log.append({"now": state.now, "n": d.n_candidates,
                             "key": [d.cost, d.finish, d.priority, d.serial], "action": action})

@@ -20,18 +20,22 @@ from __future__ import annotations
 
 import importlib
 
-from .engine import HostState
 from .instance_io import action_as, action_from, as_instance, is_reference_instance
 from .model import Schedule, SchedulingError, TimedAction
+from .state import State
 
 
 def drive(instance, chooser, policy: str, metadata: dict, prelude=()) -> Schedule:
-    """The reference decision loop (rlmux/scheduler.py:925-950).
+    """The reference decision loop (rlmux/scheduler.py:925-950) with a
+    Python chooser over the native state (used by the multi-GPU chooser,
+    dist.ShardedChooser, and by tests with the CPU oracle's chooser). The
+    single-GPU path runs this loop inside the library (`lookahead_schedule`
+    -> Evaluator.schedule -> rlx_drive).
 
     `chooser(state)` returns the action to apply now, or None when there is
     no candidate (the reference's `chooser(state, cands) if cands else None`).
     """
-    state = HostState(instance)
+    state = State(instance)
     actions = []
     for action in prelude:
         actions.append(TimedAction(state.now, action))
@@ -69,7 +73,14 @@ def lookahead_schedule(instance, window: int = 3, prelude=(), *, max_merge: int 
     ev = evaluator if evaluator is not None else Evaluator(inst)
     if ev.instance is not inst:
         ev.bind(inst)
-    sched = drive(inst, ev.chooser(window, max_merge), "lookahead", {"window": str(window)}, pre)
+    state = State(inst)
+    actions = []
+    for action in pre:
+        actions.append(TimedAction(state.now, action))
+        state.apply(action)
+    steps = ev.schedule(state, window, max_merge)  # the _drive loop, natively
+    actions += [TimedAction(t, a) for t, a in state.replay_steps(steps)]
+    sched = Schedule(actions=actions, policy="lookahead", metadata={"window": str(window)})
     if ref:
         mod = _ref_schedule_module(instance)
         sched = mod.Schedule(actions=[mod.TimedAction(t.start, action_as(t.action, mod)) for t in sched.actions],

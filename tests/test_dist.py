@@ -50,7 +50,7 @@ def _worker(rank, world, port, name, window, cap, q):
 
     from oracle.oracle import Oracle
     from paper_2604_23838_b200.dist import WORDS, minloc_allreduce
-    from paper_2604_23838_b200.engine import HostState
+    from paper_2604_23838_b200.state import State as HostState
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -74,7 +74,7 @@ def test_two_rank_decision_matches_single(name, window, cap):
     from helpers import instance
 
     from oracle.oracle import Oracle
-    from paper_2604_23838_b200.engine import HostState
+    from paper_2604_23838_b200.state import State as HostState
 
     inst = instance(name)
     want = Oracle(inst, nthreads=2).score(HostState(inst), window, cap)["best"]

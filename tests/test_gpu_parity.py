@@ -7,7 +7,7 @@ import pytest
 
 from helpers import instance, load_gz
 from paper_2604_23838_b200 import drive, simulate
-from paper_2604_23838_b200.engine import HostState
+from paper_2604_23838_b200.state import State as HostState
 from paper_2604_23838_b200.instance_io import action_to_json
 from paper_2604_23838_b200.model import SchedulingError
 

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "twi
 
 from helpers import instance  # noqa: E402
 from paper_2604_23838_b200 import drive  # noqa: E402
-from paper_2604_23838_b200.engine import HostState  # noqa: E402
+from paper_2604_23838_b200.state import State as HostState  # noqa: E402
 from paper_2604_23838_b200.instance_io import action_to_json  # noqa: E402
 
 

@@ -49,14 +49,10 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
   clip(0, dp.n_mux, wd.b0, wd.nb);
   clip(dp.n_mux + dp.n_merge, dp.n_total, wd.c0, wd.nc);
   wd.shard0 = b;
-  unsigned long long counter = 0;
-  int derr[8] = {0};
-  double dbg[16] = {0};
+  unsigned long long counter = 0, err_key = ~0ull;
   wd.counter = &counter;
-  wd.err = &derr[0];
-  wd.dbg_flag = &derr[4];
+  wd.err_key = &err_key;
   wd.keys_out = keys_out;
-  wd.dbg = dbg;
   if (dp.W > 32) {
     snprintf(err, errlen, "the host twin runs one lane: at most 32 workers (NL %d NT %d NC %d hot %u max_ord %d NTW %d)",
              dp.NL, dp.NT, dp.NC, dp.hot_bytes, dp.max_ord, dp.NTW);
@@ -74,7 +70,13 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
   key_out[1] = out.k1;
   key_out[2] = out.k2;
   key_out[3] = out.passes;
-  if (dbg_out) memcpy(dbg_out, dbg, sizeof dbg);
-  if (derr[0]) snprintf(err, errlen, "device error %d", derr[0]);
-  return derr[0];
+  if (dbg_out) {
+    dbg_out[0] = err_key == ~0ull ? -1.0 : (double)(err_key >> 8);
+    dbg_out[1] = err_key == ~0ull ? 0.0 : (double)(err_key & 0xff);
+  }
+  if (err_key != ~0ull) {
+    snprintf(err, errlen, "candidate %llu failed with device code %llu", err_key >> 8, err_key & 0xff);
+    return (err_key & 0xff) == RLX_ERR_SCHEDULING ? RLX_ERR_SCHEDULING : RLX_ERR_KEY;
+  }
+  return 0;
 }

@@ -6,7 +6,7 @@ import subprocess
 import numpy as np
 
 from paper_2604_23838_b200 import abi
-from paper_2604_23838_b200.encode import InstanceEncoding, StateEncoding
+from paper_2604_23838_b200.encode import instance_encoding
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "_build", "librlx_twin.so")
@@ -28,11 +28,10 @@ def lib():
 
 class Twin:
     def __init__(self, instance):
-        self.enc = InstanceEncoding(instance)
-        self.senc = StateEncoding(self.enc)
+        self.enc = instance_encoding(instance)
 
     def decide(self, state, window, max_merge=None, shard=(0, -1), want_keys=True):
-        sd = self.senc.encode(state)
+        sd = state.snapshot()
         n = C.c_int64()
         key = (C.c_uint64 * 4)()
         dbg = (C.c_double * 16)()

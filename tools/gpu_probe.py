@@ -5,7 +5,7 @@ import time
 sys.path.insert(0, "/root/repo")
 sys.path.insert(0, "/root/repo/tests")
 from helpers import instance  # noqa: E402
-from paper_2604_23838_b200.engine import HostState  # noqa: E402
+from paper_2604_23838_b200.state import State as HostState  # noqa: E402
 from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 
 CFG = {1: (1, None), 2: (2, None), 3: (3, 3), 4: (3, 3), 5: (4, 3), 52: (4, 2), 42: (3, 2)}

@@ -7,7 +7,7 @@ import sys
 sys.path.insert(0, "/root/repo")
 sys.path.insert(0, "/root/repo/tests")
 from helpers import instance  # noqa: E402
-from paper_2604_23838_b200.engine import HostState  # noqa: E402
+from paper_2604_23838_b200.state import State as HostState  # noqa: E402
 from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 
 cfg = sys.argv[1]

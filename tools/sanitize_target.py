@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, "/root/repo")
 sys.path.insert(0, "/root/repo/tests")
 from helpers import instance  # noqa: E402
-from paper_2604_23838_b200.engine import HostState  # noqa: E402
+from paper_2604_23838_b200.state import State as HostState  # noqa: E402
 from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 
 for name, w, cap, shard in (("trap", 3, None, None), ("config2", 2, 3, (0, 400)), ("config3", 3, 3, (8000, 8100)),
