@@ -1,6 +1,6 @@
 """Benchmark of the B200 look-ahead chooser (the north-star hot path).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config config2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config config5_cap2] [--impl ours|reference]
 
 A *step* is one look-ahead decision: every candidate of the decision state
 (enumerate_actions, rlmux/scheduler.py:648-703) is scored by the W-round
@@ -8,30 +8,36 @@ list-scheduling simulation (candidate_cost + action_finish_estimate,
 :773-918) and the (cost, finish, priority, serial) argmin is taken
 (:963-972). The workload is the FIRST decision of the named config
 (tests/golden/instances/<config>.json.gz, built with the reference's own
-generator), default config 2 = BASELINE.json configs[1]:
-2 multiplexed sync pipelines (8B + 14B), 16 simulated GPUs, 1,024
-rollouts, depth 2, long-tail migration on, uncapped merges -> 1,048,864
-candidates per decision.
+generator). Default: config 5 (BASELINE.json configs[4]:
+8 pipelines, 64 simulated GPUs, 64k rollouts, depth 4) with merge sets
+capped at 2 members — the largest decision that completes in the
+reference: at cap 3 the reference itself raises SchedulingError on serial
+819010 (a livelocking merge follow-up; tests/golden/livelock.json), which
+the device reproduces. 64,814 candidates (32,046 multiplex, 32,256 merges,
+512 exclusive), ~10.3M list-scheduling passes, ~1.2e10 simulated events.
 
 Reported (one JSON line on rank 0):
   value      candidates evaluated / s, whole job, plan resident in HBM
              (RLX_F_REUSE_PLAN: scoring kernel + argmin + cross-GPU min-loc),
              CUDA events on the launching stream, max over ranks
   e2e        the same metric through the public chooser (the `_drive` seam):
-             host state encode -> plan -> H2D -> kernel -> D2H -> action
+             host state -> plan -> H2D -> kernel -> D2H -> action
   roofline   SURVEY §8(d) algorithmic bytes of the scoring kernel per launch
              / its CUDA-event duration, against the measured HBM copy peak
-  cpu_baseline  the CPU oracle port (oracle/rlx_oracle.c, all host threads)
-             on a bounded random sample of the same decision's candidates
+  cpu_baseline  the CPU port of the reference chooser (oracle/rlx_oracle.c,
+             all host threads), class-stratified sample of the same decision
+             with a fixed budget (--cpu-seconds), extrapolated to the decision
 
-With N>1 (torchrun, NCCL) the global serial range is split into N
-contiguous shards and the shard winners meet in ONE all-reduce per
-decision (paper_2604_23838_b200/dist.py), i.e. weak-in-hardware,
-strong-in-work scaling ("strong": the decision is fixed).
+With N>1 (torchrun, NCCL) the serial range is split into N cost-balanced
+shards and the shard winners meet in ONE all-reduce per decision
+(paper_2604_23838_b200/dist.py): strong scaling (the decision is fixed).
 
-`--impl reference` times the reference algorithm on the host cores: the C
-restatement in oracle/ (the reference is pure Python and has no native
-build, so the port is the reference arm), rank 0 only.
+`--impl reference` times the reference algorithm on the host cores (rank 0
+only): the C restatement in oracle/ (the reference is pure Python with no
+native build; the port is ~100x faster per candidate than the Python, so
+it is the stricter baseline), plus the unmodified Python reference itself
+(rlmux installed into baseline/_ref) on a non-merge sample, forked over all
+cores, reported as `python_reference` with its keys checked against the port.
 """
 
 from __future__ import annotations
@@ -139,9 +145,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_sample(inst, state, window, cap, n_total, seconds, seed=0):
-    """Score a bounded uniform random sample of the decision's candidates on
-    the CPU oracle with every host thread; returns (cand/s, n, threads, s)."""
+def class_ranges(n_mux, n_merge, n_excl):
+    """Serial ranges of the three candidate classes (enumerate_actions order:
+    multiplex, merges, exclusive; scheduler.py:648-703)."""
+    return {"multiplex": (0, n_mux), "merge": (n_mux, n_mux + n_merge),
+            "exclusive": (n_mux + n_merge, n_mux + n_merge + n_excl)}
+
+
+# share of the CPU budget per class (merges cost 3(1+F) passes, the others 3)
+_CLASS_SHARE = {"merge": 0.6, "multiplex": 0.3, "exclusive": 0.1}
+
+
+def cpu_stratified(inst, state, window, cap, counts, seconds, seed=0):
+    """Class-stratified timing of the CPU port (oracle/rlx_oracle.c) on every
+    host thread, with a fixed budget of `seconds` that does not depend on
+    --steps. Per class: batches of uniformly drawn candidates (a multiple of
+    the thread count, doubling while the budget allows); the class's wall
+    time per candidate t_c includes batch stragglers, as a real parallel CPU
+    chooser pays them. The decision estimate is sum_c n_c * t_c, so
+    rate = n_total / that (extrapolated from the sample)."""
     import numpy as np
 
     from oracle.oracle import Oracle
@@ -149,19 +171,122 @@ def cpu_sample(inst, state, window, cap, n_total, seconds, seed=0):
     threads = os.cpu_count() or 1
     o = Oracle(inst, nthreads=threads)
     rng = np.random.default_rng(seed)
-    # one-batch warm-up, then batches of uniformly drawn candidates until
-    # about `seconds` of scoring (every thread busy in every batch)
-    o.score(state, window, cap, serials=np.sort(rng.choice(n_total, size=min(threads, n_total), replace=False)))
-    perm = rng.permutation(n_total) if n_total <= 4_000_000 else rng.choice(n_total, 4_000_000, replace=False)
-    n, dt, batch = 0, 0.0, threads
-    while dt < seconds and n < len(perm):
-        part = np.sort(perm[n:n + batch])
-        t = time.perf_counter()
-        o.score(state, window, cap, serials=part, want_keys=True)
-        dt += time.perf_counter() - t
-        n += len(part)
-        batch = min(batch * 2, 64 * threads)
-    return n / dt, n, threads, dt
+    ranges = class_ranges(*counts)
+    live = {c: r for c, r in ranges.items() if r[1] > r[0]}
+    share = sum(_CLASS_SHARE[c] for c in live)
+    per_class = {}
+    est = 0.0
+    for c, (lo, hi) in live.items():
+        budget = seconds * _CLASS_SHARE[c] / share
+        n_c = hi - lo
+        pool = rng.permutation(n_c)[: 1 << 20] + lo if n_c <= 8 << 20 else rng.choice(n_c, 1 << 20) + lo
+        used, wall, batch, last = 0, 0.0, threads, 0.0
+        while used < len(pool) and (used == 0 or wall + 2 * last <= budget):
+            part = np.sort(pool[used:used + batch])
+            t = time.perf_counter()
+            o.score(state, window, cap, serials=part, want_keys=True)
+            last = time.perf_counter() - t
+            wall += last
+            used += len(part)
+            batch = min(batch * 2, 64 * threads)
+        t_c = wall / used
+        per_class[c] = {"candidates": n_c, "sampled": used, "wall_s": wall, "wall_s_per_candidate": t_c}
+        est += n_c * t_c
+    n_total = sum(counts)
+    return {"rate": n_total / est, "decision_s": est, "threads": threads, "classes": per_class,
+            "sampled": sum(v["sampled"] for v in per_class.values()),
+            "wall_s": sum(v["wall_s"] for v in per_class.values())}
+
+
+def cpu_baseline_record(r, n_total, kind="port"):
+    parts = ", ".join(f"{c} {v['sampled']}/{v['candidates']} ({v['wall_s_per_candidate'] * 1e3:.3g} ms/cand wall)"
+                      for c, v in r["classes"].items())
+    return {"value": r["rate"], "unit": "candidates/s", "cores": r["threads"], "kind": kind,
+            "sample": f"class-stratified sample of the {n_total}-candidate decision ({parts}), scored by "
+                      f"oracle/rlx_oracle.c on {r['threads']} host threads in {r['wall_s']:.1f} s ({cpu_model()}); "
+                      f"value = n_total / sum_c n_c * t_c (extrapolated decision time {r['decision_s']:.1f} s)"}
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+_PYREF = {}
+
+
+def _pyref_init(inst, window):
+    import rlmux.scheduler as rsch
+
+    from paper_2604_23838_b200.instance_io import to_reference
+
+    ri = to_reference(inst)
+    _PYREF.update(inst=ri, state=rsch.ExecState(ri), window=window, mod=rsch)
+
+
+def _pyref_score(action_json):
+    """The reference chooser's work for one non-merge candidate
+    (scheduler.py:963-972: candidate_cost + action_finish_estimate)."""
+    from paper_2604_23838_b200.instance_io import action_as, action_from_json
+
+    rsch = _PYREF["mod"]
+    a = action_as(action_from_json(action_json), rsch)
+    t = time.perf_counter()
+    cost = rsch.candidate_cost(_PYREF["state"], a, _PYREF["window"])
+    fin = rsch.action_finish_estimate(_PYREF["state"], a)
+    return time.perf_counter() - t, cost, fin
+
+
+def python_reference_sample(inst, state, window, cap, counts, seconds, seed=1):
+    """The UNMODIFIED reference (rlmux installed in baseline/_ref from
+    /root/reference) scoring a uniform sample of the decision's non-merge
+    candidates, forked over every host core, next to the C port on the same
+    candidates (one thread). Merges are not sampled: one config-5 merge
+    costs ~20 min of single-core Python. Returns per-candidate thread
+    seconds of both, the key agreement, and the port/Python ratio."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    if not os.path.isdir(os.path.join(REF_DIR, "rlmux")):
+        return {"unavailable": "baseline/_ref/rlmux not installed"}
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from oracle.oracle import Oracle
+    from paper_2604_23838_b200.instance_io import action_to_json
+
+    procs = os.cpu_count() or 1
+    n_mux, n_merge, n_excl = counts
+    rng = np.random.default_rng(seed)
+    pool_serials = np.concatenate([rng.permutation(n_mux), n_mux + n_merge + rng.permutation(n_excl)])
+    pool_serials = rng.permutation(pool_serials)[:4096]
+    o1 = Oracle(inst, nthreads=1)
+    ctx = mp.get_context("fork")
+    done, wall, times, keys = 0, 0.0, [], []
+    with ctx.Pool(procs, initializer=_pyref_init, initargs=(inst, window)) as pool:
+        last = 0.0
+        while done < len(pool_serials) and (done == 0 or wall + last <= seconds):
+            part = [int(x) for x in pool_serials[done:done + procs]]
+            acts = [action_to_json(o1.candidate(state, s, cap)) for s in part]
+            t = time.perf_counter()
+            res = pool.map(_pyref_score, acts, chunksize=1)
+            last = time.perf_counter() - t
+            wall += last
+            times += [r[0] for r in res]
+            keys += [(s, r[1], r[2]) for s, r in zip(part, res)]
+            done += len(part)
+    sample = sorted(k[0] for k in keys)
+    t = time.perf_counter()
+    r = o1.score(state, window, cap, serials=sample, want_keys=True)
+    port_s = time.perf_counter() - t
+    port = {s: tuple(k) for s, k in zip(sample, r["keys"])}
+    agree = all(port[s] == (c, f) for s, c, f in keys)
+    py_t = sum(times) / len(times)
+    port_t = port_s / len(sample)
+    return {"kind": "reference (rlmux, unmodified, baseline/_ref)", "procs": procs,
+            "sample": f"{len(sample)} uniformly drawn multiplex/exclusive candidates, forked over {procs} processes "
+                      f"in {wall:.1f} s",
+            "python_thread_s_per_candidate": py_t, "port_thread_s_per_candidate": port_t,
+            "port_speedup_over_python": py_t / port_t, "keys_match_port": agree,
+            "candidates_per_s_nonmerge": procs / py_t}
 
 
 def cpu_model():
@@ -231,41 +356,37 @@ def schedule_latency(name, device, cpu=False, max_decisions=None):
 
 
 def run_reference(args):
+    """The reference arm: the CPU port of the reference chooser on every host
+    thread (class-stratified, fixed budget --cpu-seconds independent of
+    --steps), plus the unmodified Python reference (baseline/_ref) on a
+    non-merge sample next to the port. Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    from oracle.oracle import Oracle
     from paper_2604_23838_b200.state import State as HostState
 
     window, cap, desc = CONFIGS[args.config]
     inst = load_instance(args.config)
     st = HostState(inst)
-    from oracle.oracle import Oracle
-
-    n_total = Oracle(inst, nthreads=1).score(st, window, cap, serials=[])["n"]
-    rates = []
-    last = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds / max(args.steps, 1), seed=i)
-        if i >= args.warmup:
-            rates.append(r)
-        last = r
+    counts = Oracle(inst, nthreads=1).counts(st, window, cap)
+    n_total = sum(counts)
+    r = cpu_stratified(inst, st, window, cap, counts, args.cpu_seconds)
+    value = r["rate"]
     sched = (schedule_latency(args.schedule_config, 0, cpu=True, max_decisions=args.schedule_decisions)
              if args.schedule_p50 else None)
-    tot_n = sum(r[1] for r in rates)
-    tot_s = sum(r[3] for r in rates)
-    value = tot_n / tot_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / len(rates),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["decision_s"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, golden instance)",
         "config": {"workload": f"{args.config} first decision: {desc}", "window": window, "max_merge": cap,
                    "candidates_per_decision": n_total},
-        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": last[2], "kind": "port",
-                         "sample": f"{last[1]} uniformly sampled candidates of the {n_total}-candidate decision "
-                                   f"per step, scored by oracle/rlx_oracle.c on {last[2]} threads ({cpu_model()})"},
+        "cpu_baseline": cpu_baseline_record(r, n_total),
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.python_seconds > 0:
+        line["python_reference"] = python_reference_sample(inst, st, window, cap, counts, args.python_seconds)
     if sched is not None:
         line["schedule"] = sched
     print(json.dumps(line), flush=True)
@@ -362,8 +483,8 @@ def run_ours(args):
         # ---- e2e through the public chooser (host state in, action out)
         choose = ev.chooser(window, cap, group=dist.group.WORLD if world > 1 else None)
         e2e_ms, wall_ms = [], []
-        e2e_steps = max(args.steps, 3)
-        for i in range(args.warmup + e2e_steps):
+        e2e_steps = min(max(args.steps, 3), args.e2e_steps)
+        for i in range(1 + e2e_steps):  # one warm-up (the plan is the same decision)
             flush.fill_(i)
             torch.cuda.synchronize(dev)
             barrier()
@@ -375,7 +496,7 @@ def run_ours(args):
             a1.record(stream)
             torch.cuda.synchronize(dev)
             w = (time.perf_counter() - t) * 1e3
-            if i >= args.warmup:
+            if i >= 1:
                 e2e_ms.append(a0.elapsed_time(a1))
                 wall_ms.append(w)
         last_e2e = ev.last
@@ -404,10 +525,8 @@ def run_ours(args):
         sched = schedule_latency(args.schedule_config, local, max_decisions=args.schedule_decisions)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, n, threads, secs = cpu_sample(inst, st, window, cap, n_total, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "candidates/s", "cores": threads, "kind": "port",
-               "sample": f"{n} uniformly sampled candidates of the {n_total}-candidate decision, scored by "
-                         f"oracle/rlx_oracle.c on {threads} host threads in {secs:.1f} s ({cpu_model()})"}
+        counts = (d0.n_multiplex, d0.n_merge, d0.n_exclusive)
+        cpu = cpu_baseline_record(cpu_stratified(inst, st, window, cap, counts, args.cpu_seconds), n_total)
     winner = sorted(winners)
     line = {
         "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world, "steps": args.steps,
@@ -455,9 +574,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("RLX_BENCH_CONFIG", "config2"), choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=os.environ.get("RLX_BENCH_CONFIG", "config5_cap2"), choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=60.0,
+                    help="fixed CPU-port budget (class-stratified), independent of --steps")
+    ap.add_argument("--python-seconds", type=float, default=40.0,
+                    help="budget of the unmodified Python reference sample (reference arm; 0 = skip)")
+    ap.add_argument("--e2e-steps", type=int, default=5, help="decisions timed through the public chooser")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--schedule-config", default="config1", choices=sorted(CONFIGS))
     ap.add_argument("--no-schedule", dest="schedule_p50", action="store_false")

@@ -113,6 +113,30 @@ class Oracle:
             a.members[i] = buf[6 + i]
         return state.action_from_raw(a)
 
+    def counts(self, state, window: int, max_merge: int | None = None):
+        """(n_multiplex, n_merge, n_exclusive) of a decision: the serial
+        space is laid out in that class order (scheduler.py:648-703), so the
+        class boundaries are found by binary search on decoded serials."""
+        n = self.score(state, window, max_merge, serials=[])["n"]
+
+        def cls(s):
+            a = self.candidate(state, s, max_merge)
+            name = type(a).__name__
+            return 0 if name == "Multiplex" else (1 if name == "Merge" else 2)
+
+        def first(at_least):
+            lo, hi = 0, n
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if cls(mid) >= at_least:
+                    hi = mid
+                else:
+                    lo = mid + 1
+            return lo
+
+        a, b = first(1), first(2)
+        return a, b - a, n - b
+
     def chooser(self, window: int, max_merge: int | None = None, log=None):
         """A `drive` chooser that decides with the oracle."""
 

@@ -193,3 +193,35 @@ def action_from_json(j):
     if j[0] == "M":
         return Multiplex(j[1], j[2], ResourceAllocation(j[3], j[4]))
     return Merge(tuple(j[1]), int(j[2]))
+
+
+def to_reference(inst: Instance):
+    """This package's Instance -> the reference's own objects (the inverse of
+    `as_instance`; needs an importable `rlmux`). Pipeline specs become
+    records of the fields the scheduling path reads (migration_cost,
+    rlmux/scheduler.py:174-182); the generator-only PipelineSpec fields
+    (stages, samples) are not part of an Instance's scheduling semantics."""
+    import types
+
+    import rlmux.graph as rg
+    import rlmux.scheduler as rsch
+    import rlmux.slowdown as rsl
+
+    graphs = []
+    for g in inst.graphs:
+        nodes = {nid: rg.SubStage(id=n.id, pipeline_id=n.pipeline_id, worker_id=n.worker_id,
+                                  kind=rg.SubStageKind(n.kind.value), duration=n.duration,
+                                  mem_fraction=n.mem_fraction, step_span=tuple(n.step_span),
+                                  sample_ids=frozenset(n.sample_ids),
+                                  remaining_decode_tokens=n.remaining_decode_tokens,
+                                  active_requests=n.active_requests, context_tokens=n.context_tokens,
+                                  token_total=n.token_total) for nid, n in g.nodes.items()}
+        spec = None if g.spec is None else types.SimpleNamespace(
+            pipeline_id=g.pipeline_id, model_params=g.spec.model_params,
+            device_peak_flops=g.spec.device_peak_flops, prefill_mfu=g.spec.prefill_mfu)
+        graphs.append(rg.SubStageGraph(g.pipeline_id, nodes, set(g.edges), spec, dict(g.latency_model)))
+    entries = {(rg.SubStageKind(k.value), None if p is None else rg.SubStageKind(p.value), a, m): f
+               for (k, p, a, m), f in inst.model.table.entries.items()}
+    return rsch.Instance(graphs=graphs, model=rsl.SlowdownModel(rsl.SlowdownTable(entries)),
+                         headroom=inst.headroom, realloc_penalty=inst.realloc_penalty,
+                         default_migration_cost=inst.default_migration_cost, merge_enabled=inst.merge_enabled)

@@ -24,3 +24,11 @@ def golden_keys():
 @pytest.fixture(scope="session")
 def golden_schedules_knobs():
     return load_gz("schedules_knobs.json.gz")
+
+
+@pytest.fixture(scope="session")
+def Evaluator():
+    """The device chooser class (librlx.so through the C-ABI)."""
+    from paper_2604_23838_b200.native import Evaluator as E
+
+    return E

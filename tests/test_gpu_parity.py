@@ -20,13 +20,6 @@ pytestmark = pytest.mark.gpu
 LIVELOCK = {"config4": 84807, "config5": 819010}
 
 
-@pytest.fixture(scope="module")
-def Evaluator():
-    from paper_2604_23838_b200.native import Evaluator as E
-
-    return E
-
-
 def test_golden_schedules(Evaluator, golden_schedules):
     bad = []
     ev = None
@@ -154,8 +147,11 @@ def test_livelock_matches_oracle(Evaluator, cfg, window):
     ev = Evaluator(inst)
     with pytest.raises(SchedulingError) as ei:
         ev.decide(st, window, 3, shard=None if cfg == "config4" else (serial - 3000, serial + 3000))
-    named = int(str(ei.value).split("serial ")[1].split()[0])
-    for s in sorted({serial, named}):
+    # the lowest livelocking serial (the one the reference's serial scan
+    # raises on) rides on the exception; the message is the reference's text
+    assert ei.value.serial == serial
+    assert str(ei.value) == "window estimate did not converge"
+    for s in [serial]:
         with pytest.raises(SchedulingError):
             ev.decide(st, window, 3, shard=(s, s + 1))
         with pytest.raises(OracleError):

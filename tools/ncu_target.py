@@ -1,6 +1,6 @@
 """One warm-up + one measured decision at a config (ncu target).
 
-    python tools/ncu_target.py <config> <window> <cap|none> [n_serials]
+    python tools/ncu_target.py <config> <window> <cap|none> [n_serials | begin:end]
 """
 import sys
 
@@ -13,7 +13,10 @@ from paper_2604_23838_b200.native import Evaluator  # noqa: E402
 cfg = sys.argv[1]
 w = int(sys.argv[2])
 cap = None if sys.argv[3] == "none" else int(sys.argv[3])
-shard = (0, int(sys.argv[4])) if len(sys.argv) > 4 else None
+shard = None
+if len(sys.argv) > 4:
+    a = sys.argv[4]
+    shard = tuple(int(x) for x in a.split(":")) if ":" in a else (0, int(a))
 inst = instance(cfg)
 ev = Evaluator(inst)
 st = HostState(inst)
