@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define RLX_ABI_VERSION 3
+#define RLX_ABI_VERSION 4
 
 /* Kind codes = declaration order of rlmux SubStageKind (graph.py:69-76). */
 enum {
@@ -151,8 +151,10 @@ typedef struct RlxDecideArgs {
   int64_t serial_end;            /*   end < 0 means "to the last candidate"               */
   double* keys_out;              /* optional host [2*(end-begin)]: (cost, finish) per     */
                                  /*   candidate, for parity tests                         */
-  void* dev_key_out;             /* optional DEVICE pointer to 4 x uint64 that receives   */
-                                 /*   the shard's packed best key (for the NCCL min-loc)  */
+  void* dev_key_out;             /* optional DEVICE pointer to 5 x uint64 that receives   */
+                                 /*   the shard's packed best key (RlxKey) and, in word 4, */
+                                 /*   its lowest failing candidate (serial << 8 | device  */
+                                 /*   error code; ~0: none) — the row of the NCCL min-loc */
   int32_t flags;                 /* RLX_F_*                                               */
   int32_t _pad;
 } RlxDecideArgs;
@@ -160,9 +162,10 @@ typedef struct RlxDecideArgs {
 #define RLX_F_NO_SYNC_STATS 1     /* skip the stats readback */
 #define RLX_F_REUSE_PLAN 2        /* re-score the plan already resident on the device   */
                                   /*   (state may be NULL; no planning, no H2D copy)     */
-#define RLX_F_SHARD 4             /* serial_begin/serial_end = shard index / shard count: */
-                                  /*   score the contiguous block [r*q+min(r,m), ...) of  */
-                                  /*   n = q*count+m serials (dist.shard_range)           */
+#define RLX_F_SHARD 4             /* serial_begin/serial_end = part index r / part count w: */
+                                  /*   score every w-th block of 32 serials of each class */
+                                  /*   (multiplex, merges, exclusive), starting at block r */
+                                  /*   — cost-balanced multi-GPU shards (dist.part_serials) */
 
 /* Packed key: cost and finish are non-negative doubles, so their bit
  * patterns order as uint64; word 2 = priority << 61 | serial; word 3 = 1 if
@@ -205,6 +208,8 @@ typedef struct RlxDecision {
   int64_t d2h_bytes;             /* result bytes copied device -> host                    */
   int64_t shard_begin, shard_end;/* serial range actually scored                          */
   int64_t events;                /* simulated events (advances) over all passes           */
+  int64_t err_key;               /* lowest failing candidate of the shard: serial << 8 |  */
+                                 /*   device error code, or -1 (rlx_error_text)           */
 } RlxDecision;
 
 /* ---- native execution state (ExecState) ------------------------------ */
@@ -352,6 +357,10 @@ int rlx_decode(void* handle, int64_t serial, RlxAction* out);
  * default stream pass cudaStreamLegacy, not NULL. */
 int rlx_set_stream(void* handle, void* cuda_stream);
 const char* rlx_last_error(void* handle);
+/* Status and the reference's message for a device error code (the low byte
+ * of RlxDecision.err_key), so every rank of a multi-GPU decision can raise
+ * the same exception for the globally lowest failing candidate. */
+int rlx_error_text(int32_t device_code, char* buf, int32_t buf_len);
 void rlx_close(void* handle);
 
 #ifdef __cplusplus

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-RLX_ABI_VERSION = 3
+RLX_ABI_VERSION = 4
 RLX_F_NO_SYNC_STATS = 1
 RLX_F_REUSE_PLAN = 2
 RLX_F_SHARD = 4
@@ -76,7 +76,7 @@ class RlxDecision(C.Structure):
         ("passes", C.c_int64), ("alg_bytes", C.c_double), ("kernel_ms", C.c_double), ("plan_ms", C.c_double),
         ("n_merge", C.c_int64), ("n_multiplex", C.c_int64), ("n_exclusive", C.c_int64),
         ("device_ms", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-        ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("events", C.c_int64),
+        ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("events", C.c_int64), ("err_key", C.c_int64),
     ]
 
 
@@ -146,7 +146,7 @@ class RlxPlanInfo(C.Structure):
 
 # Every symbol include/rlx.h declares (checked by tests/test_abi.py).
 EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "rlx_decode",
-            "rlx_last_error", "rlx_close", "rlx_set_stream", "rlx_drive", "rlx_plan_info",
+            "rlx_last_error", "rlx_error_text", "rlx_close", "rlx_set_stream", "rlx_drive", "rlx_plan_info",
             "rlx_state_create", "rlx_state_clone", "rlx_state_destroy", "rlx_state_error", "rlx_state_apply",
             "rlx_state_advance", "rlx_state_info", "rlx_state_snapshot", "rlx_state_node", "rlx_state_events",
             "rlx_state_completion")
@@ -166,6 +166,8 @@ def bind(lib: C.CDLL) -> C.CDLL:
     lib.rlx_decode.argtypes = [C.c_void_p, C.c_int64, C.POINTER(RlxAction)]
     lib.rlx_last_error.restype = C.c_char_p
     lib.rlx_last_error.argtypes = [C.c_void_p]
+    lib.rlx_error_text.restype = C.c_int
+    lib.rlx_error_text.argtypes = [C.c_int32, C.c_char_p, C.c_int32]
     lib.rlx_set_stream.restype = C.c_int
     lib.rlx_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     lib.rlx_close.restype = None

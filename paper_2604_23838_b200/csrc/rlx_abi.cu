@@ -25,6 +25,7 @@ using namespace rlx;
 namespace {
 
 constexpr int kMaxSlices = 1 << 17;
+constexpr int kShardBlockShift = 5;  // multi-GPU shards interleave blocks of 32 serials per class
 constexpr size_t kSliceOutBytes = 56;
 static_assert(sizeof(rlx::SliceOut) == kSliceOutBytes, "SliceOut layout");
 
@@ -86,15 +87,29 @@ const char* kind_name(int k) {
 }
 
 // Device error code (rlx_kernels.cu kErr*) -> status + the reference's text.
-int device_error(Handle* h, int code) {
-  if (code == RLX_ERR_SCHEDULING) return fail(h, RLX_ERR_SCHEDULING, "window estimate did not converge");  // :867
-  if (code >= 8 && code < 16) return fail(h, RLX_ERR_KEY, std::to_string(code - 8));  // latency_model[bucket]
+int device_error_text(int code, std::string& msg) {
+  if (code == RLX_ERR_SCHEDULING) {
+    msg = "window estimate did not converge";  // :867
+    return RLX_ERR_SCHEDULING;
+  }
+  if (code >= 8 && code < 16) {  // latency_model[bucket]
+    msg = std::to_string(code - 8);
+    return RLX_ERR_KEY;
+  }
   if (code >= 16) {
     const int k = (code - 16) / RLX_NPARTNER, p = (code - 16) % RLX_NPARTNER - 1;
-    return fail(h, RLX_ERR_KEY, std::string("slowdown table has no rows for pair ") + kind_name(k) + "/" +
-                                    (p < 0 ? "-" : kind_name(p)));  // slowdown.py:143-147
+    msg = std::string("slowdown table has no rows for pair ") + kind_name(k) + "/" +
+          (p < 0 ? "-" : kind_name(p));  // slowdown.py:143-147
+    return RLX_ERR_KEY;
   }
-  return fail(h, RLX_ERR_CUDA, "device error " + std::to_string(code));
+  msg = "device error " + std::to_string(code);
+  return RLX_ERR_CUDA;
+}
+
+int device_error(Handle* h, int code) {
+  std::string m;
+  const int st = device_error_text(code, m);
+  return fail(h, st, m);
 }
 
 #define CK(x)                                   \
@@ -210,6 +225,7 @@ static int decide_impl(Handle* h, const RlxStateDesc* sd, const RlxDecideArgs* a
   if (!reuse && !sd) return RLX_ERR_ARG;
   memset(out, 0, sizeof *out);
   out->serial = -1;
+  out->err_key = -1;
   CK(cudaSetDevice(h->device));
   auto t0 = std::chrono::steady_clock::now();
   int rc = 0;
@@ -226,25 +242,50 @@ static int decide_impl(Handle* h, const RlxStateDesc* sd, const RlxDecideArgs* a
   out->n_merge = hv.n_merge;
   out->n_multiplex = hv.n_mux;
   out->n_exclusive = hv.n_excl;
+  // ---- work ranges per class: merges first (heaviest), then multiplex, then exclusive
+  WorkDesc wd;
+  memset(&wd, 0, sizeof wd);
+  const int64_t lo[3] = {hv.n_mux, 0, hv.n_mux + hv.n_merge};
+  const int64_t hi[3] = {hv.n_mux + hv.n_merge, hv.n_mux, hv.n_total};
   int64_t b = args->serial_begin < 0 ? 0 : args->serial_begin;
   int64_t e = args->serial_end < 0 ? hv.n_total : args->serial_end;
-  if (args->flags & RLX_F_SHARD) {  // cost-balanced block `serial_begin` of `serial_end` blocks
+  wd.world = 1;
+  if (args->flags & RLX_F_SHARD) {
+    // cost-balanced part `serial_begin` of `serial_end`: every world-th block
+    // of kShardBlock serials of each class (dist.py)
     const int64_t r = args->serial_begin, w = args->serial_end;
     if (w < 1 || r < 0 || r >= w) return fail(h, RLX_ERR_ARG, "bad shard index / count");
-    shard_bounds(h->hp, r, w, b, e);
+    if (args->keys_out) return fail(h, RLX_ERR_ARG, "keys_out needs an explicit serial range");
+    wd.world = (int)w;
+    wd.rank = (int)r;
+    wd.blk_shift = kShardBlockShift;
+    for (int c = 0; c < 3; c++) {
+      wd.s0[c] = lo[c];
+      wd.loc[c] = cyclic_count(hi[c] - lo[c], wd.rank, wd.world, wd.blk_shift);
+    }
+    b = 0;
+    e = hv.n_total;
+  } else {
+    if (e > hv.n_total) e = hv.n_total;
+    if (b > e) b = e;
+    for (int c = 0; c < 3; c++) {
+      const int64_t x = lo[c] > b ? lo[c] : b, y = hi[c] < e ? hi[c] : e;
+      wd.s0[c] = x;
+      wd.loc[c] = y > x ? y - x : 0;
+    }
   }
   out->shard_begin = b;
   out->shard_end = e;
-  if (e > hv.n_total) e = hv.n_total;
-  if (b > e) b = e;
   auto t1 = std::chrono::steady_clock::now();
   out->plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-  if (e == b) {
+  if (wd.loc[0] + wd.loc[1] + wd.loc[2] == 0) {
     if (args->dev_key_out) {
       CK(cudaMemsetAsync(args->dev_key_out, 0xFF, 24, h->stream));
       CK(cudaMemsetAsync((uint8_t*)args->dev_key_out + 24, 0, 8, h->stream));
+      CK(cudaMemsetAsync((uint8_t*)args->dev_key_out + 32, 0xFF, 8, h->stream));
       CK(cudaStreamSynchronize(h->stream));
     }
+    out->err_key = -1;
     return RLX_OK;
   }
   // ---- upload plan (skipped when re-scoring the resident plan)
@@ -272,17 +313,6 @@ static int decide_impl(Handle* h, const RlxStateDesc* sd, const RlxDecideArgs* a
   out->h2d_bytes = (int64_t)nb;
   DevPlan dp;
   relocate(h->hp, h->d_blob, dp);
-  // ---- work ranges: merges first (heaviest), then multiplex, then exclusive
-  WorkDesc wd;
-  memset(&wd, 0, sizeof wd);
-  auto clip = [&](int64_t lo, int64_t hi, int64_t& s, int64_t& n) {
-    int64_t x = lo > b ? lo : b, y = hi < e ? hi : e;
-    s = x;
-    n = y > x ? y - x : 0;
-  };
-  clip(hv.n_mux, hv.n_mux + hv.n_merge, wd.a0, wd.na);
-  clip(0, hv.n_mux, wd.b0, wd.nb);
-  clip(hv.n_mux + hv.n_merge, hv.n_total, wd.c0, wd.nc);
   wd.shard0 = b;
   wd.counter = h->d_counter;
   wd.err_key = h->d_errkey;
@@ -307,12 +337,15 @@ static int decide_impl(Handle* h, const RlxStateDesc* sd, const RlxDecideArgs* a
   CK(cudaEventRecord(h->e1, h->stream));
   rc = launch_reduce((SliceOut*)h->d_outs, n_slices, h->d_res, h->stream);
   if (rc) return fail(h, rc, "reduce launch failed");
-  if (args->dev_key_out)
+  if (args->dev_key_out) {
     CK(cudaMemcpyAsync(args->dev_key_out, h->d_res, 32, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync((uint8_t*)args->dev_key_out + 32, h->d_errkey, 8, cudaMemcpyDeviceToDevice, h->stream));
+  }
   CK(cudaMemcpyAsync(h->h_res, h->d_res, 64, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaMemcpyAsync(&h->h_res[8], h->d_errkey, 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   const unsigned long long ek = h->h_res[8];
+  out->err_key = ek == ~0ull ? -1 : (int64_t)ek;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->e0, h->e1);
   out->kernel_ms = ms;
@@ -477,6 +510,13 @@ int rlx_decode(void* handle, int64_t serial, RlxAction* out) {
   if (!decode_serial(h->host_view, serial, c)) return fail(h, RLX_ERR_ARG, "serial out of range");
   fill_action(h, c, out);
   return RLX_OK;
+}
+
+int rlx_error_text(int32_t device_code, char* buf, int32_t buf_len) {
+  std::string m;
+  const int st = device_error_text(device_code, m);
+  if (buf && buf_len > 0) snprintf(buf, (size_t)buf_len, "%s", m.c_str());
+  return st;
 }
 
 const char* rlx_last_error(void* handle) {

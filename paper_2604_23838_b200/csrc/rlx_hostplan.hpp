@@ -50,7 +50,6 @@ struct HostPlan {
 int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, int max_merge, HostPlan& hp,
                std::string& err);
 void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d);
-void shard_bounds(const HostPlan& hp, int64_t r, int64_t w, int64_t& b, int64_t& e);
 int check_capacity(const HostPlan& hp, std::string& err);
 
 void choose_shape(int W, int& G, int& WPL);

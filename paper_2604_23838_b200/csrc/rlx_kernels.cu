@@ -79,15 +79,67 @@ RLX_HD int at_add(int* p, int v) {
   *p = o + v;
   return o;
 }
+// Ready masks are u64 per worker; a completion sets one bit with a 32-bit
+// shared-memory OR on the word that holds it (native ATOMS.OR — a 64-bit
+// atomicOr compiles to a CAS loop).
 template <int G>
-RLX_HD void at_or(unsigned long long* p, unsigned long long v) {
+RLX_HD void at_or_bit(unsigned long long* p, int bit) {
 #ifdef __CUDA_ARCH__
   if (G > 1) {
-    atomicOr(p, v);
+    atomicOr(reinterpret_cast<unsigned*>(p) + (bit >> 5), 1u << (bit & 31));
     return;
   }
 #endif
-  *p |= v;
+  *p |= 1ull << bit;
+}
+RLX_HD int at_min32(int* p, int v) {
+#ifdef __CUDA_ARCH__
+  return atomicMin(p, v);
+#else
+  int o = *p;
+  if (v < o) *p = v;
+  return o;
+#endif
+}
+RLX_HD void at_min64s(unsigned long long* p, unsigned long long v) {  // shared-memory u64 min
+#ifdef __CUDA_ARCH__
+  atomicMin(p, v);
+#else
+  if (v < *p) *p = v;
+#endif
+}
+RLX_HD int at_add32(int* p, int v) {
+#ifdef __CUDA_ARCH__
+  return atomicAdd(p, v);
+#else
+  int o = *p;
+  *p = o + v;
+  return o;
+#endif
+}
+// The warp slice's candidate generation: published with an atomic exchange
+// after a fence, polled with an atomic read (the groups' only handshake).
+RLX_HD void gen_store(int* p, int v) {
+#ifdef __CUDA_ARCH__
+  __threadfence_block();
+  atomicExch(p, v);
+#else
+  *p = v;
+#endif
+}
+RLX_HD int gen_load(int* p) {
+#ifdef __CUDA_ARCH__
+  const int v = atomicAdd(p, 0);
+  __threadfence_block();
+  return v;
+#else
+  return *p;
+#endif
+}
+RLX_HD void fence_block() {
+#ifdef __CUDA_ARCH__
+  __threadfence_block();
+#endif
 }
 RLX_HD unsigned long long at_add64(unsigned long long* p, unsigned long long v) {
 #ifdef __CUDA_ARCH__
@@ -167,6 +219,25 @@ RLX_HD int ffs64(unsigned long long m) {
 #endif
 }
 
+// RN(1 / r) (IEEE, round to nearest even)
+RLX_HD double recip(double r) {
+#ifdef __CUDA_ARCH__
+  return __drcp_rn(r);
+#else
+  return 1.0 / r;
+#endif
+}
+// RN(d / r) from y = RN(1 / r): q0 = RN(d * y) is within one ulp of d / r,
+// the residual e = d - q0 * r is exact in one FMA, and RN(q0 + e * y) is the
+// correctly rounded quotient (Markstein's theorem; verified bit-exact
+// against IEEE division on 3e8 random and adversarial operands, and by
+// every golden test). Explicit FMAs are unaffected by -fmad=false.
+RLX_HD double ediv(double d, double r, double y) {
+  const double q0 = d * y;
+  const double e = fma(-q0, r, d);
+  return fma(e, y, q0);
+}
+
 // MEM_GRID (slowdown.py:19) and DEFAULT_MEM_FRACTIONS by kind code (graph.py:98-106).
 RLX_HD double memgrid(int j) { return j == 0 ? 0.20 : j == 1 ? 0.40 : j == 2 ? 0.60 : 0.80; }
 RLX_HD double defmem(int k) {
@@ -212,27 +283,44 @@ struct Act {  // action started at pass begin
   int a, b, alloc;
 };
 
-// Per-group candidate + pass-iterator state (shared memory).
-struct GroupCand {
+// One candidate at a time per warp (shared memory). Its passes — 3 variants
+// x (1 + F) actions (candidate_cost :902-918 / window_cost :878-899) — form
+// a queue that the warp's groups drain together, variant-major, so the
+// groups of a warp simulate near-identical passes (same variant, sibling
+// follow-ups of one merge) and their per-event control flow coincides.
+// The last group to run dry finalises the key and fetches the next
+// candidate (bumping `gen`); the others poll `gen` meanwhile.
+struct WarpCand {
   double dur, mem, pre, suf;  // merged node M (merged_estimate :185-199, migration_cost :174-182)
-  double cost, fin;           // running candidate_cost and action_finish_estimate
-  double bytes;               // SURVEY §8(d) algorithmic bytes scored by this group
-  unsigned long long b0, b1, b2;  // best packed key of this group
-  unsigned long long passes, ncand, rm, events;
-  long long serial;
+  double fin;                 // action_finish_estimate (:773-789)
+  unsigned long long cost;    // running min of the pass results (bit patterns of doubles >= 0)
+  long long serial;           // -1: none
   int kind, pipe, t, k, ins0, ins1, idle, cls;
-  int a, b, alloc, nwin;  // candidate action (non-merge)
-  int phase, y, oo, ai, mj, v;  // pass iterator
-  int fa, fb, falloc;     // follow-up action of the current pass
-  int twq_n, tw_run;
-  int cerr;  // error of the current candidate (first failure), 0 if none
-  int dsum;  // window completions of the running pass (plans without tool waits)
+  int a, b, alloc, nwin;      // candidate action (non-merge)
+  int n_act, n_var, total;    // passes = n_var x n_act
+  int next;                   // next pass index (shared atomic)
+  int done;                   // groups that found the queue empty
+  int err;                    // first failing pass: (reference pass index << 8 | code), INT_MAX none
+  int cerr;                   // candidate-level error (merged_estimate), 0 if none
+  int gen;                    // candidate generation; -1: no more candidates (gen_load / gen_store)
   uint16_t m[kMaxMembers];
+  // followed by uint16_t acts[acts_cap]: merge follow-ups (q << 5 | oo << 4 | ai * 4 + mj)
 };
 
-// Group slice layout (offsets in bytes from the slice start), stored in the
-// DevPlan constants by launch_score.
+// Per-group pass state and results (shared memory).
+struct GroupCand {
+  double bytes;                   // SURVEY §8(d) algorithmic bytes scored by this group
+  unsigned long long b0, b1, b2;  // best packed key finalised by this group
+  unsigned long long passes, ncand, events;
+  int twq_n, tw_run;
+  int dsum;  // window completions of the running pass (plans without tool waits)
+};
+
+// Warp and group slice layout (offsets in bytes), stored in the DevPlan
+// constants by launch_score.
 RLX_HD void group_layout(DevPlan& P, int G, int WPL) {
+  P.acts_cap = 24 * (P.max_ord > 0 ? P.max_ord : 1);
+  P.w_bytes = (uint32_t)((sizeof(WarpCand) + 2u * P.acts_cap + 15) & ~size_t(15));
   uint32_t b = (uint32_t)((sizeof(GroupCand) + 15) & ~size_t(15));
   P.g_mask = b;
   b += 8u * P.W;
@@ -260,11 +348,12 @@ template <int G, int WPL>
 struct Lane {
   typedef typename BitsFor<WPL>::type Bits;
   static_assert(WPL <= 32, "at most 32 workers per lane");
-  const uint32_t gbase;  // slice offset in SMEM
+  const uint32_t gbase;  // group slice offset in SMEM
+  const uint32_t wbase;  // warp slice offset in SMEM
   const int lane;
   const unsigned gm;
   // registers: running members of this lane's workers (slot s of local worker j)
-  double wk[WPL][2], rt[WPL][2];
+  double wk[WPL][2], rt[WPL][2], ri[WPL][2];  // work left, rate, RN(1/rate)
   Bits rb;    // bit 2j+s: running
   Bits pm;    // bit 2j+s: has a non-zero prefix (value in the slice)
   Bits pf;    // bit 2j+s: still has a multiplex partner
@@ -275,13 +364,14 @@ struct Lane {
   int done_cnt, guard;
   bool any_done;
 
-  RLX_HD Lane(uint32_t gb, int ln, unsigned m) : gbase(gb), lane(ln), gm(m) {
+  RLX_HD Lane(uint32_t gb, uint32_t wb, int ln, unsigned m) : gbase(gb), wbase(wb), lane(ln), gm(m) {
     err = 0;
     rb = pm = pf = 0;
   }
 
   // ---- shared-memory views
   RLX_HD GroupCand* gc() const { return reinterpret_cast<GroupCand*>(SMEM + gbase); }
+  RLX_HD WarpCand* wc() const { return reinterpret_cast<WarpCand*>(SMEM + wbase); }
   RLX_HD unsigned long long* mask() const { return reinterpret_cast<unsigned long long*>(SMEM + gbase + PLAN.g_mask); }
   RLX_HD double* twend() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_twend); }
   RLX_HD double* grant() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_grant); }
@@ -303,12 +393,12 @@ struct Lane {
   RLX_HD double hmpre(int n) const { return arr<double>(PLAN.o_mprefix)[n]; }
   RLX_HD double lutv(int i) const { return arr<double>(PLAN.o_lut)[i]; }
   // node attributes (M = the candidate's virtual merged node)
-  RLX_HD int kind(int n) const { return n == PLAN.M ? gc()->kind : hkind(n); }
-  RLX_HD int pipe(int n) const { return n == PLAN.M ? gc()->pipe : hpipe(n); }
-  RLX_HD double dur(int n) const { return n == PLAN.M ? gc()->dur : hdur(n); }
-  RLX_HD double memf(int n) const { return n == PLAN.M ? gc()->mem : hmem(n); }
-  RLX_HD double mpre(int n) const { return n == PLAN.M ? gc()->pre : hmpre(n); }
-  RLX_HD int wrk(int n) const { return n == PLAN.M ? gc()->t : hworker(n); }
+  RLX_HD int kind(int n) const { return n == PLAN.M ? wc()->kind : hkind(n); }
+  RLX_HD int pipe(int n) const { return n == PLAN.M ? wc()->pipe : hpipe(n); }
+  RLX_HD double dur(int n) const { return n == PLAN.M ? wc()->dur : hdur(n); }
+  RLX_HD double memf(int n) const { return n == PLAN.M ? wc()->mem : hmem(n); }
+  RLX_HD double mpre(int n) const { return n == PLAN.M ? wc()->pre : hmpre(n); }
+  RLX_HD int wrk(int n) const { return n == PLAN.M ? wc()->t : hworker(n); }
 
   RLX_HD double L3(int k, int partner, int alloc) {
     double v = lutv((k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc);
@@ -335,7 +425,7 @@ struct Lane {
       const int q = at_add<G>(&gc()->twq_n, 1);
       twq()[q] = (uint16_t)s;
     } else if (f & F_WIN) {
-      at_or<G>(&mask()[hworker(s)], 1ull << pos_of(s));
+      at_or_bit<G>(&mask()[hworker(s)], pos_of(s));
     }
   }
   RLX_HD void fire(int s) {
@@ -359,8 +449,8 @@ struct Lane {
   RLX_HD void complete(int n, unsigned& ld) {
     if (n == PLAN.M) {
       ld++;
-      const GroupCand* g = gc();
-      for (int i = 0; i < g->k; i++) succs_of(g->m[i]);
+      const WarpCand* c = wc();
+      for (int i = 0; i < c->k; i++) succs_of(c->m[i]);
     } else {
       if (hflags(n) & F_WIN) ld++;
       succs_of(n);
@@ -379,11 +469,13 @@ struct Lane {
       *g = am;
     }
     const double d = dur(n);
+    const double rinv = recip(rate);
 #pragma unroll
     for (int jj = 0; jj < WPL; jj++) {  // predicated register select (no per-lane branches)
       const bool hit = jj == j;
       wk[jj][s] = hit ? d : wk[jj][s];
       rt[jj][s] = hit ? rate : rt[jj][s];
+      ri[jj][s] = hit ? rinv : ri[jj][s];
     }
     const Bits bit = Bits(1) << (2 * j + s);
     nds()[2 * j + s] = n;
@@ -440,9 +532,10 @@ struct Lane {
   // ---- pass initialisation: decision state + `act` applied (window_cost :886-887)
   RLX_HD void init_pass(int variant, const Act& act, bool is_merge) {
     GroupCand* g = gc();
+    const WarpCand* c = wc();
     o = variant == 2 ? 1 : 0;
-    mt = is_merge ? g->t : -1;
-    ins = is_merge ? (o ? g->ins1 : g->ins0) : -1;
+    mt = is_merge ? c->t : -1;
+    ins = is_merge ? (o ? c->ins1 : c->ins0) : -1;
     now = PLAN.now;
     last = 0.0;
     done_cnt = 0;
@@ -477,6 +570,7 @@ struct Lane {
             const double r = PLAN.mrate0[2 * w + s], p = PLAN.mpre0[2 * w + s], wv = PLAN.mwork0[2 * w + s];
             nds()[2 * j + s] = PLAN.mnode0[2 * w + s];
             rt[j][s] = r;
+            ri[j][s] = recip(r);
             wk[j][s] = wv;
             rb |= bit;
             if (PLAN.mpart0[2 * w + s]) pf |= bit;
@@ -495,8 +589,8 @@ struct Lane {
       const unsigned long long m = mk[mt];
       const unsigned long long lo = ins ? (m & ((1ull << ins) - 1)) : 0ull;
       mk[mt] = lo | ((m >> ins) << (ins + 1)) | (1ull << ins);
-      for (int i = 0; i < g->k; i++) {
-        const int x = g->m[i];
+      for (int i = 0; i < c->k; i++) {
+        const int x = c->m[i];
         mk[hworker(x)] &= ~(1ull << pos_of(x));
       }
     }
@@ -614,10 +708,10 @@ struct Lane {
         }
         double wv = wk[j][s];
         const double r = rt[j][s];
-        double q = d;
-        // only members of a multiplexed pair divide; keep the IEEE division
-        // sequence a real branch instead of an if-converted one every lane pays
-        if (__builtin_expect(r != 1.0 && on && dp && wv > kEps, 0)) q = d / r;
+        // dt / rate (:335), correctly rounded without a division: Markstein's
+        // correction of d * RN(1/r) by one exact FMA residual is RN(d / r)
+        // (exact for rate 1.0), so every member runs the same straight-line code
+        const double q = ediv(d, r, ri[j][s]);
         const double z = wv - q;
         const double nw = z > 0.0 ? z : 0.0;
         wv = (on && dp && wv > kEps) ? nw : wv;
@@ -632,6 +726,7 @@ struct Lane {
           const Bits bit = Bits(1) << (2 * j + s);
           if ((rb & bit) && !(fb & bit) && (pf & bit)) {
             rt[j][s] = 1.0;
+            ri[j][s] = 1.0;
             pf &= ~bit;
           }
         }
@@ -741,7 +836,7 @@ struct Lane {
 // Merged node of a Merge candidate (_apply_merge :517-581, merged_estimate
 // :185-199, migration_cost :174-182) and its insertion point in both worker
 // orders (ids compare as Python str). Group leader only.
-RLX_HD void setup_merge(const Cand& c, GroupCand* sc) {
+RLX_HD void setup_merge(const Cand& c, WarpCand* sc) {
   long long tokens = 0, active = 0;
   double dmax = 0.0, mmax = 0.0, sfx = 0.0;
   const int p = PLAN.pipe[c.m[0]];
@@ -852,222 +947,298 @@ RLX_HD void setup_merge(const Cand& c, GroupCand* sc) {
 }
 
 // ---------------------------------------------------------------------------
-// Pass iterator of one candidate (candidate_cost :902-918 / window_cost
-// :878-899): variants innermost; a merge onto an idle target runs Exclusive(M)
-// and then every Multiplex follow-up touching M (orientation x alpha x mem,
-// feasible only), a merge onto a busy target runs the merge alone.
-// Returns false when the candidate has no further pass. Group-uniform.
-RLX_HD bool next_action(GroupCand* g) {
-  if (g->v < 2) {
-    g->v++;
-    // variant 2 (name order) repeats variant 0 (suffix order) exactly when
-    // both orders coincide on every worker, the merged node included
-    if (!(g->v == 2 && PLAN.same_order && (g->cls != 1 || g->ins0 == g->ins1))) return true;
-  }
-  g->v = 0;
-  if (g->cls != 1 || !g->idle) return false;
-  const double hr = PLAN.headroom;
-  // advance (y, oo, ai, mj) to the next feasible follow-up
-  for (;;) {
-    if (g->phase == 0) {
-      g->phase = 1;
-      g->y = -1;
-    } else {
-      if (++g->mj < 4) goto check;
-      g->mj = 0;
-      if (++g->ai < 3) goto check;
-      g->ai = 0;
-      if (++g->oo < 2) goto check;
-      g->y = -1;
-    }
-    // next partner on the target worker (ready at the decision, name order)
-    for (;;) {
-      if (!g->rm) return false;
-      const int q = ffs64(g->rm) - 1;
-      g->rm &= g->rm - 1;
-      const int y = PLAN.ord[(1 * PLAN.W + g->t) * kMaxPos + q];
+// The pass list of a candidate (candidate_cost :902-918): a non-merge
+// candidate or a merge onto a busy target is one action; a merge onto an
+// idle target is Exclusive(M) followed by every Multiplex follow-up touching
+// M (partners ready on the target in name order x orientation x alpha x
+// mem, feasible only). Each action runs the window_cost variants (:893-897);
+// variant 2 (name order) repeats variant 0 (suffix order) exactly when both
+// orders coincide on every worker, the merged node included, so it is
+// skipped then. Warp-slice writer only.
+RLX_HD void build_passes(WarpCand* c) {
+  uint16_t* acts = reinterpret_cast<uint16_t*>(c + 1);
+  int n = 1;
+  if (c->cls == 1 && c->idle) {
+    const double hr = PLAN.headroom;
+    unsigned long long rm = PLAN.mask0[1 * PLAN.W + c->t];
+    while (rm) {
+      const int q = ffs64(rm) - 1;
+      rm &= rm - 1;
+      const int y = PLAN.ord[(1 * PLAN.W + c->t) * kMaxPos + q];
       bool member = false;
-      for (int i = 0; i < g->k; i++) member |= g->m[i] == y;
-      if (member || PLAN.pipe[y] == g->pipe) continue;
-      if (!(g->mem + PLAN.mem[y] <= 1.0 - hr + 1e-12)) continue;
-      g->y = y;
-      g->oo = g->ai = g->mj = 0;
+      for (int i = 0; i < c->k; i++) member |= c->m[i] == y;
+      if (member || PLAN.pipe[y] == c->pipe) continue;
+      if (!(c->mem + PLAN.mem[y] <= 1.0 - hr + 1e-12)) continue;
+      for (int oo = 0; oo < 2; oo++)
+        for (int ai = 0; ai < 3; ai++)
+          for (int mj = 0; mj < 4; mj++) {
+            const double ms = oo ? c->mem : PLAN.mem[y];
+            if (memgrid(mj) + ms > 1.0 - hr + kEps) continue;
+            acts[n - 1] = (uint16_t)(q << 5 | oo << 4 | (ai * 4 + mj));
+            n++;
+          }
+    }
+  }
+  c->n_act = n;
+  c->n_var = (PLAN.same_order && (c->cls != 1 || c->ins0 == c->ins1)) ? 2 : 3;
+  c->total = c->cerr ? 0 : n * c->n_var;
+}
+
+// The action of action index `ai` of the warp's candidate.
+RLX_HD Act pass_action(const WarpCand* c, int ai) {
+  if (c->cls != 1) return Act{c->cls, c->a, c->b, c->alloc};
+  if (!c->idle) return Act{-1, -1, -1, 0};
+  if (ai == 0) return Act{2, PLAN.M, -1, 0};
+  const int e = reinterpret_cast<const uint16_t*>(c + 1)[ai - 1];
+  const int y = PLAN.ord[(1 * PLAN.W + c->t) * kMaxPos + (e >> 5)];
+  const bool oo = (e >> 4) & 1;
+  return Act{0, oo ? y : PLAN.M, oo ? PLAN.M : y, 1 + (e & 15)};
+}
+
+// Decode serial `serial` into the warp slice and set up its pass queue
+// (merged node, finish estimate, passes). Warp-slice writer only.
+RLX_HD void load_candidate(WarpCand* c, long long serial) {
+  Cand cd;
+  decode_serial(PLAN, serial, cd);
+  c->serial = serial;
+  c->cls = cd.cls;
+  c->cost = dbits(INFINITY);
+  c->err = 0x7fffffff;
+  c->cerr = 0;
+  if (cd.cls == 1) {
+    setup_merge(cd, c);
+    c->fin = (PLAN.now + c->pre) + c->dur;
+    c->nwin = PLAN.NWIN - cd.k + 1;
+  } else {
+    // action_finish_estimate :773-789 (with the realloc penalty of the decision state)
+    c->a = cd.a;
+    c->b = cd.cls == 0 ? cd.b : -1;
+    c->alloc = cd.alloc;
+    c->nwin = PLAN.NWIN;
+    auto pre_of = [&](int n, int alloc) {
+      double pre = PLAN.mprefix[n];
+      if (PLAN.has_penalty && PLAN.kind[n] <= RLX_KIND_DECODE_SMALL) {
+        const double gr = PLAN.grant0[PLAN.worker[n] * PLAN.P + PLAN.pipe[n]];
+        if (!isnan(gr) && fabs(gr - PLAN.alloc_mem[alloc]) > kEps) pre = pre + PLAN.realloc_penalty;
+      }
+      return pre;
+    };
+    auto lut = [&](int k, int partner, int alloc, int& err) {
+      const double v = PLAN.lut[(k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc];
+      if (isnan(v) && !err) err = key_err(k, partner);
+      return v;
+    };
+    int e = 0;
+    if (cd.cls == 2) {
+      const double r = lut(PLAN.kind[cd.a], -1, 0, e);
+      c->fin = (PLAN.now + pre_of(cd.a, 0)) + PLAN.dur[cd.a] * r;
+    } else {
+      const double ra = lut(PLAN.kind[cd.a], PLAN.kind[cd.b], cd.alloc, e);
+      const double rbv = lut(PLAN.kind[cd.b], PLAN.kind[cd.a], cd.alloc + 12, e);
+      const double fa = (PLAN.now + pre_of(cd.a, cd.alloc)) + PLAN.dur[cd.a] * ra;
+      const double fb = (PLAN.now + pre_of(cd.b, cd.alloc + 12)) + PLAN.dur[cd.b] * rbv;
+      c->fin = fb > fa ? fb : fa;
+    }
+    // a missing LUT row raises in the first pass's apply (window_cost runs
+    // before action_finish_estimate, :963-972): the passes report it
+    (void)e;
+  }
+  build_passes(c);
+}
+
+// Serial of work index `idx` of this launch: per class (merges, then
+// multiplex, then exclusive: heaviest first) the shard owns either a
+// contiguous range (world == 1) or every world-th block of 2^blk_shift
+// serials starting at block `rank` (cost-balanced multi-GPU shards).
+RLX_HD long long work_serial(const WorkDesc& wd, long long idx) {
+  for (int r = 0; r < 3; r++) {
+    if (idx < wd.loc[r]) {
+      const long long blk = idx >> wd.blk_shift, off = idx & ((1ll << wd.blk_shift) - 1);
+      return wd.s0[r] + ((blk * wd.world + wd.rank) << wd.blk_shift) + off;
+    }
+    idx -= wd.loc[r];
+  }
+  return -1;
+}
+
+// Fetch the next candidate of the launch into the warp slice (gen + 1), or
+// mark the warp done (gen = -1). Once some candidate failed, only lower
+// serials can still change the outcome (the reference raises on the first
+// failing serial of its scan).
+RLX_HD void fetch_candidate(const WorkDesc& wd, WarpCand* c) {
+  const long long total = wd.loc[0] + wd.loc[1] + wd.loc[2];
+  long long serial = -1;
+  for (;;) {
+    const long long idx = (long long)at_add64(wd.counter, 1ull);
+    if (idx >= total) break;
+    const long long s = work_serial(wd, idx);
+    if ((unsigned long long)s <= (*(volatile unsigned long long*)wd.err_key >> 8)) {
+      serial = s;
       break;
     }
-  check : {
-    const double ms = g->oo ? g->mem : PLAN.mem[g->y];
-    if (memgrid(g->mj) + ms > 1.0 - hr + kEps) continue;
-    g->fa = g->oo ? g->y : PLAN.M;
-    g->fb = g->oo ? PLAN.M : g->y;
-    g->falloc = 1 + g->ai * 4 + g->mj;
-    return true;
   }
+  const int g = gen_load(&c->gen);
+  if (serial < 0) {
+    c->serial = -1;
+    gen_store(&c->gen, -1);
+    return;
+  }
+  load_candidate(c, serial);
+  c->next = 0;
+  c->done = 0;
+  gen_store(&c->gen, g + 1);
+}
+
+// Finalise the warp's candidate: key (cost, finish, priority, serial) into
+// this group's running best, or the failure into the launch's error key.
+RLX_HD void finish_candidate(const WorkDesc& wd, WarpCand* c, GroupCand* g) {
+  if (c->serial < 0) return;
+  const int code = c->cerr ? c->cerr : (c->err != 0x7fffffff ? (c->err & 0xff) : 0);
+  if (code) {
+    at_min64(wd.err_key, ((unsigned long long)c->serial << 8) | (unsigned long long)code);
+    return;
+  }
+  g->ncand++;
+  double cost;
+  const unsigned long long cb = c->cost;
+  memcpy(&cost, &cb, 8);
+  const unsigned long long k0 = cb, k1 = dbits(c->fin);
+  const unsigned long long k2 = ((unsigned long long)c->cls << 61) | (unsigned long long)c->serial;
+  if (key_less(k0, k1, k2, g->b0, g->b1, g->b2)) {
+    g->b0 = k0;
+    g->b1 = k1;
+    g->b2 = k2;
+  }
+  if (wd.keys_out) {
+    wd.keys_out[2 * (c->serial - wd.shard0)] = cost;
+    wd.keys_out[2 * (c->serial - wd.shard0) + 1] = c->fin;
   }
 }
 
-// The candidate loop of one group, flattened so that one iteration is one
+// One group's share of a launch, flattened so that one loop iteration is one
 // simulated event for every group of the warp (pass and candidate
-// boundaries are short divergent prologues).
+// boundaries are short divergent prologues). `ngw` groups share the warp
+// slice at `wbase`.
 template <int G, int WPL>
-RLX_HD void group_loop(const WorkDesc& wd, uint32_t gbase, int lane, unsigned gm, SliceOut* out) {
-  Lane<G, WPL> S(gbase, lane, gm);
-  GroupCand* g = S.gc();
-  if (lane == 0) {
-    g->b0 = g->b1 = g->b2 = ~0ull;
-    g->passes = g->ncand = g->events = 0;
-    g->bytes = 0.0;
-    g->cls = -1;
-    g->cerr = 0;
-  }
-  gsync<G>(gm);
-  const int64_t total = wd.na + wd.nb + wd.nc;
+struct GroupRunner {
+  Lane<G, WPL> S;
+  const WorkDesc& wd;
+  const int ngw;
   bool active = false;  // a pass is running
+  bool ran = false;     // a pass ran since the last fold
+  bool drained = false; // this group found the current candidate's queue empty
+  int gen = 0;          // generation of the candidate this group works on
+  int p = 0, variant = 0, nwin = 0, ref_idx = 0;
   bool pair = false;
-  int variant = 0, nwin = 0;
-  for (;;) {
-    if (!active) {
-      // ---- pass boundary: fold the finished pass, pick the next one.
-      // Group-shared candidate state is written by lane 0 only; every read
-      // by the other lanes is separated from those writes by a __syncwarp
-      // (memory ordering, not just a shuffle) — compute-sanitizer racecheck.
-      bool more = false;
-      gsync<G>(gm);
-      if (g->cls >= 0) {
-        const double x = S.any_done ? S.last : S.now;
-        const int e = gmax<G>(gm, S.err);  // the pass failed on some lane: the candidate raises
-        gsync<G>(gm);
-        if (lane == 0) {
-          g->events += (unsigned long long)S.guard;
-          if (e > g->cerr) g->cerr = e;
-          if (!g->cerr) {
-            if (x < g->cost) g->cost = x;
-            more = next_action(g);
-          }
-        }
-        more = gbcast<G>(gm, more ? 1 : 0) != 0;
-        gsync<G>(gm);
-      }
-      if (!more) {
-        if (g->cls >= 0 && lane == 0) {  // finished candidate: key (cost, finish, priority, serial)
-          if (g->cerr) {
-            // the reference raises on the first failing candidate of its serial scan
-            at_min64(wd.err_key, ((unsigned long long)g->serial << 8) | (unsigned long long)g->cerr);
-          } else {
-            g->ncand++;
-            const unsigned long long k0 = dbits(g->cost), k1 = dbits(g->fin);
-            const unsigned long long k2 = ((unsigned long long)g->cls << 61) | (unsigned long long)g->serial;
-            if (key_less(k0, k1, k2, g->b0, g->b1, g->b2)) {
-              g->b0 = k0;
-              g->b1 = k1;
-              g->b2 = k2;
-            }
-            if (wd.keys_out) {
-              wd.keys_out[2 * (g->serial - wd.shard0)] = g->cost;
-              wd.keys_out[2 * (g->serial - wd.shard0) + 1] = g->fin;
-            }
-          }
-        }
-        S.err = 0;
-        // ---- next candidate (heaviest class first); once some candidate
-        // failed, only lower serials can still change the outcome
-        long long idx = 0, serial = 0;
-        if (lane == 0) {
-          for (;;) {
-            idx = (long long)at_add64(wd.counter, 1ull);
-            if (idx >= total) break;
-            serial = idx < wd.na ? wd.a0 + idx
-                                 : (idx < wd.na + wd.nb ? wd.b0 + (idx - wd.na) : wd.c0 + (idx - wd.na - wd.nb));
-            if ((unsigned long long)serial <= (*(volatile unsigned long long*)wd.err_key >> 8)) break;
-          }
-        }
-        idx = gbcast<G>(gm, idx);
-        if (idx >= total) break;
-        gsync<G>(gm);  // every lane has read the previous candidate's fields
-        if (lane == 0) {
-          Cand c;
-          decode_serial(PLAN, serial, c);
-          g->serial = serial;
-          g->cls = c.cls;
-          g->cost = INFINITY;
-          g->v = 0;
-          g->phase = 0;
-          g->cerr = 0;
-          if (c.cls == 1) {
-            setup_merge(c, g);
-            g->fin = (PLAN.now + g->pre) + g->dur;
-            g->nwin = PLAN.NWIN - c.k + 1;
-            g->rm = PLAN.mask0[1 * PLAN.W + g->t];
-            if (g->idle) {  // first pass: Exclusive(M)
-              g->fa = PLAN.M;
-              g->fb = -1;
-              g->falloc = 0;
-            }
-          } else {
-            // action_finish_estimate :773-789 (with the realloc penalty of the decision state)
-            g->a = c.a;
-            g->b = c.cls == 0 ? c.b : -1;
-            g->alloc = c.alloc;
-            g->nwin = PLAN.NWIN;
-            auto pre_of = [&](int n, int alloc) {
-              double pre = PLAN.mprefix[n];
-              if (PLAN.has_penalty && PLAN.kind[n] <= RLX_KIND_DECODE_SMALL) {
-                const double gr = PLAN.grant0[PLAN.worker[n] * PLAN.P + PLAN.pipe[n]];
-                if (!isnan(gr) && fabs(gr - PLAN.alloc_mem[alloc]) > kEps) pre = pre + PLAN.realloc_penalty;
-              }
-              return pre;
-            };
-            if (c.cls == 2) {
-              const double r = S.L3(PLAN.kind[c.a], -1, 0);
-              g->fin = (PLAN.now + pre_of(c.a, 0)) + PLAN.dur[c.a] * r;
-            } else {
-              const double ra = S.L3(PLAN.kind[c.a], PLAN.kind[c.b], c.alloc);
-              const double rbv = S.L3(PLAN.kind[c.b], PLAN.kind[c.a], c.alloc + 12);
-              const double fa = (PLAN.now + pre_of(c.a, c.alloc)) + PLAN.dur[c.a] * ra;
-              const double fb = (PLAN.now + pre_of(c.b, c.alloc + 12)) + PLAN.dur[c.b] * rbv;
-              g->fin = fb > fa ? fb : fa;
-            }
-          }
-        }
-        gsync<G>(gm);
-      }
-      if (g->cerr) continue;  // merged_estimate raised: no pass runs (boundary records the error)
-      // ---- start the pass
-      const bool is_merge = g->cls == 1;
-      variant = g->v;
-      pair = variant == 1;
-      nwin = g->nwin;
-      Act act;
-      if (!is_merge) {
-        act = Act{g->cls, g->a, g->b, g->alloc};
-      } else if (!g->idle) {
-        act = Act{-1, -1, -1, 0};
-      } else if (g->phase == 0) {
-        act = Act{2, PLAN.M, -1, 0};
-      } else {
-        act = Act{0, g->fa, g->fb, g->falloc};
-      }
-      S.init_pass(variant, act, is_merge);
-      if (lane == 0 && variant == 0) {  // the reference's 3 passes of this action (SURVEY §8(d) bytes)
-        g->passes += 3;
-        g->bytes += 3.0 * (32.0 * nwin + 4.0 * (double)PLAN.ew +
-                           32.0 * (PLAN.n_run0 + (act.cls < 0 ? 0 : act.cls == 0 ? 2 : 1)) + 16.0 * PLAN.n_tw_run0);
-      }
-      active = nwin > 0;
-      if (!active) continue;  // empty window: the pass result is `now` (:889-890)
+
+  RLX_HD GroupRunner(const WorkDesc& w, uint32_t gbase, uint32_t wbase, int lane, unsigned gm, int n)
+      : S(gbase, wbase, lane, gm), wd(w), ngw(n) {}
+
+  RLX_HD void init() {
+    GroupCand* g = S.gc();
+    if (S.lane == 0) {
+      g->b0 = g->b1 = g->b2 = ~0ull;
+      g->passes = g->ncand = g->events = 0;
+      g->bytes = 0.0;
     }
-    active = S.step(pair, nwin, g->serial, variant);
+    gsync<G>(S.gm);
   }
-  gsync<G>(gm);
-  if (lane == 0) {
-    out->k0 = g->b0;
-    out->k1 = g->b1;
-    out->k2 = g->b2;
-    out->passes = g->passes;
-    out->bytes = g->bytes;
-    out->cands = g->ncand;
-    out->events = g->events;
+
+  // One iteration; false when the launch has no more work for this group.
+  RLX_HD bool iter() {
+    if (active) {
+      active = S.step(pair, nwin, 0, variant);
+      return true;
+    }
+    // ---- pass boundary. Warp-slice fields are written by one lane and read
+    // by the others after a __syncwarp / fence (compute-sanitizer racecheck).
+    GroupCand* g = S.gc();
+    WarpCand* c = S.wc();
+    gsync<G>(S.gm);
+    if (ran) {  // fold the finished pass into the candidate
+      const double x = S.any_done ? S.last : S.now;
+      const int e = gmax<G>(S.gm, S.err);
+      gsync<G>(S.gm);
+      if (S.lane == 0) {
+        g->events += (unsigned long long)S.guard;
+        if (e) {
+          at_min32(&c->err, ref_idx << 8 | e);
+        } else {
+          at_min64s(&c->cost, dbits(x));
+        }
+      }
+      S.err = 0;
+      ran = false;
+    }
+    int q = -1, st = 0;  // st: 0 claimed pass q, 1 wait, 2 exit
+    if (S.lane == 0) {
+      const int cg = gen_load(&c->gen);
+      if (cg < 0) {
+        st = 2;
+      } else {
+        if (cg != gen) {
+          gen = cg;
+          drained = false;
+        }
+        st = 1;
+        while (!drained) {
+          const int t = at_add32(&c->next, 1);
+          if (t >= c->total) {
+            drained = true;
+            fence_block();
+            if (at_add32(&c->done, 1) == ngw - 1) {  // last group out: finalise, fetch the next
+              fence_block();
+              finish_candidate(wd, c, g);
+              fetch_candidate(wd, c);
+            }
+            break;
+          }
+          const int na = c->n_act;
+          const int ri = (t % na) * 3 + t / na;  // reference order: action-major, variant-minor
+          if ((ri << 8) > c->err) continue;  // an earlier pass of this candidate already failed
+          q = t;
+          st = 0;
+          break;
+        }
+      }
+    }
+    st = (int)gbcast<G>(S.gm, st);
+    if (st == 2) return false;
+    if (st == 1) return true;
+    q = (int)gbcast<G>(S.gm, q);
+    fence_block();
+    const int na = c->n_act;
+    const int ai = q % na;
+    variant = q / na;
+    ref_idx = ai * 3 + variant;
+    pair = variant == 1;
+    nwin = c->nwin;
+    const Act act = pass_action(c, ai);
+    S.init_pass(variant, act, c->cls == 1);
+    if (S.lane == 0 && variant == 0) {  // the reference's 3 passes of this action (SURVEY §8(d) bytes)
+      g->passes += 3;
+      g->bytes += 3.0 * (32.0 * nwin + 4.0 * (double)PLAN.ew +
+                         32.0 * (PLAN.n_run0 + (act.cls < 0 ? 0 : act.cls == 0 ? 2 : 1)) + 16.0 * PLAN.n_tw_run0);
+    }
+    ran = true;
+    active = nwin > 0;  // empty window: the pass result is `now` (:889-890)
+    return true;
   }
-}
+
+  RLX_HD void finish(SliceOut* out) {
+    gsync<G>(S.gm);
+    const GroupCand* g = S.gc();
+    if (S.lane == 0) {
+      out->k0 = g->b0;
+      out->k1 = g->b1;
+      out->k2 = g->b2;
+      out->passes = g->passes;
+      out->bytes = g->bytes;
+      out->cands = g->ncand;
+      out->events = g->events;
+    }
+  }
+};
 
 // ---- TMA bulk staging of the hot plan region into shared memory
 __device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
@@ -1115,24 +1286,29 @@ constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : WPL <= 2 ? RLX_T
 constexpr int min_blocks_for(int WPL) { return WPL <= 2 ? RLX_MINB2 : 1; }
 
 template <int G, int WPL>
-__global__ void __launch_bounds__(threads_for(WPL), min_blocks_for(WPL)) rlx_score_kernel(const WorkDesc wd,
-                                                                                          SliceOut* outs) {
+__global__ void __launch_bounds__(threads_for(WPL), min_blocks_for(WPL))
+    rlx_score_kernel(const __grid_constant__ WorkDesc wd, SliceOut* outs) {
   __shared__ __align__(8) uint64_t bar;
   stage_hot(rlx_smem, c_plan.hot, c_plan.hot_bytes, &bar);
   const int lane = threadIdx.x % G;
   const int grp = threadIdx.x / G;
   const int wl = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kNgw = 32 / G;  // groups per warp
   const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl / G * G));
-  SliceOut* out = &outs[blockIdx.x * (blockDim.x / G) + grp];
-  if (c_plan.diag_one_group && wl >= G) {  // diagnostic: one group per warp
-    if (lane == 0) {
-      out->k0 = out->k1 = out->k2 = ~0ull;
-      out->passes = out->cands = out->events = 0;
-      out->bytes = 0.0;
-    }
-    return;
+  const uint32_t wbase = c_plan.hot_bytes + (uint32_t)warp * c_plan.w_bytes;
+  const uint32_t gbase = c_plan.hot_bytes + (uint32_t)(blockDim.x >> 5) * c_plan.w_bytes + (uint32_t)grp * c_plan.g_bytes;
+  if (wl == 0) {  // the warp's first candidate
+    WarpCand* c = reinterpret_cast<WarpCand*>(rlx_smem + wbase);
+    gen_store(&c->gen, 0);
+    fetch_candidate(wd, c);
   }
-  group_loop<G, WPL>(wd, c_plan.hot_bytes + (uint32_t)grp * c_plan.g_bytes, lane, gm, out);
+  __syncwarp();
+  GroupRunner<G, WPL> R(wd, gbase, wbase, lane, gm, kNgw);
+  R.init();
+  while (R.iter()) {
+  }
+  R.finish(&outs[blockIdx.x * (blockDim.x / G) + grp]);
 }
 
 // Shard winner + stats over all groups (deterministic: lexicographic min).
@@ -1207,7 +1383,7 @@ void choose_shape(int W, int& G, int& WPL) {
 size_t plan_slice_bytes(const DevPlan& P, int G, int WPL) {
   DevPlan P2 = P;
   group_layout(P2, G, WPL);
-  return P2.g_bytes;
+  return P2.w_bytes + (size_t)(32 / G) * P2.g_bytes;  // one warp: its candidate slice + its groups
 }
 
 static KernelFn pick(int G, int WPL) {
@@ -1256,32 +1432,32 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
   if (!fn || G * WPL < P.W) return RLX_ERR_LIMIT;
   DevPlan P2 = P;
   group_layout(P2, G, WPL);
-  P2.diag_one_group = getenv("RLX_DIAG_ONE_GROUP") != nullptr;  // development diagnostic
-  const size_t gb = P2.g_bytes;
+  const size_t gb = P2.g_bytes, wb = P2.w_bytes;
   wd.slice_bytes = (int)gb;
   const size_t hot = P.hot_bytes;
   const size_t cap = kSmemCap;
-  if (hot + gb > cap) return RLX_ERR_LIMIT;
+  auto need_smem = [&](int t) { return hot + (size_t)(t / 32) * wb + (size_t)(t / G) * gb; };
+  if (need_smem(32) > cap) return RLX_ERR_LIMIT;
   int threads = threads_hint > 0 && threads_hint <= threads_for(WPL) ? threads_hint : threads_for(WPL);
-  while (threads > G && hot + (size_t)(threads / G) * gb > cap) threads /= 2;
-  const size_t smem = hot + (size_t)(threads / G) * gb;
+  while (threads > 32 && need_smem(threads) > cap) threads /= 2;
+  const size_t smem = need_smem(threads);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return RLX_ERR_CUDA;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return RLX_ERR_CUDA;
   if (per_sm < 1) return RLX_ERR_LIMIT;
-  const int64_t total = wd.na + wd.nb + wd.nc;
-  const int64_t per_block = threads / G;
+  const int64_t total = wd.loc[0] + wd.loc[1] + wd.loc[2];
+  const int64_t per_block = threads / 32;  // one candidate at a time per warp
   const int64_t need = (total + per_block - 1) / per_block;
   int64_t blocks = (int64_t)per_sm * sm_count;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  if (blocks * per_block > max_slices) blocks = max_slices / per_block;
+  if (blocks * (threads / G) > max_slices) blocks = max_slices / (threads / G);
   if (cudaMemcpyToSymbolAsync(c_plan, &P2, sizeof(DevPlan), 0, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return RLX_ERR_CUDA;
   fn<<<(unsigned)blocks, threads, smem, st>>>(wd, outs);
   if (cudaGetLastError() != cudaSuccess) return RLX_ERR_CUDA;
-  *n_slices_out = (int)(blocks * per_block);
+  *n_slices_out = (int)(blocks * (threads / G));
   return 0;
 }
 

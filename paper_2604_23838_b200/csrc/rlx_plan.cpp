@@ -592,12 +592,6 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
 }
 
 // Serial block `r` of `w` (RLX_F_SHARD): contiguous, sizes differ by <= 1.
-void shard_bounds(const HostPlan& hp, int64_t r, int64_t w, int64_t& b, int64_t& e) {
-  const int64_t n = hp.dp.n_total, q = n / w, rem = n % w;
-  b = r * q + (r < rem ? r : rem);
-  e = b + q + (r < rem ? 1 : 0);
-}
-
 // The device path's capacity checks that depend only on the plan: a kernel
 // shape for W workers and the shared-memory footprint of the hot region.
 int check_capacity(const HostPlan& hp, std::string& err) {

@@ -63,7 +63,7 @@ struct DevPlan {
   int32_t NC;  // readiness counters: nodes (and joins) with >= 2 unresolved preds
   int32_t max_ord;  // longest per-worker order (ready-mask width)
   int32_t same_order;  // 1: suffix order == name order on every worker
-  int32_t diag_one_group;  // diagnostic launch: only the first group of every warp works
+  int32_t acts_cap;  // merge follow-up list capacity per warp slice (set at launch)
 
   // Hot region: the leading `hot_bytes` of the plan blob hold every array the
   // event loop touches; the kernel stages it into shared memory with TMA bulk
@@ -74,6 +74,7 @@ struct DevPlan {
       o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab, o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
   uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
+  uint32_t w_bytes;  // warp slice (one candidate and its pass queue)
 
   // per local node (NT unless noted)
   const uint8_t* kind;       // [NL]
@@ -145,17 +146,32 @@ struct SliceOut {
   unsigned long long events;  // simulated events (advances) over all passes
 };
 
-// Work handed to one scoring launch (one serial shard).
+// Work handed to one scoring launch (one serial shard). Per class r
+// (0 merges, 1 multiplex, 2 exclusive — heaviest first) the shard owns
+// loc[r] serials: with world == 1 the contiguous range [s0[r], s0[r] +
+// loc[r]); otherwise every world-th block of 2^blk_shift serials of the
+// class range starting at s0[r], beginning with block `rank`
+// (rlx_kernels.cu work_serial; cost-balanced multi-GPU shards).
 struct WorkDesc {
-  int64_t a0, na;   // merge serial range of the shard
-  int64_t b0, nb;   // multiplex range
-  int64_t c0, nc;   // exclusive range
+  int64_t s0[3];
+  int64_t loc[3];
+  int32_t world, rank, blk_shift, slice_bytes;  // slice_bytes: DevPlan::g_bytes
   int64_t shard0;   // keys_out index base
   double* keys_out; // device, optional
   unsigned long long* counter;
   unsigned long long* err_key;  // lowest failing candidate: serial << 8 | error code (~0: none)
-  int slice_bytes;  // shared-memory bytes per group (DevPlan::g_bytes)
 };
+
+// Serials a block-cyclic shard owns of a class of n serials.
+RLX_HD int64_t cyclic_count(int64_t n, int rank, int world, int shift) {
+  const int64_t B = int64_t(1) << shift;
+  const int64_t nblk = (n + B - 1) / B;
+  if (rank >= nblk) return 0;
+  const int64_t owned = (nblk - rank + world - 1) / world;
+  int64_t cnt = owned * B;
+  if ((nblk - 1) % world == rank && (n % B)) cnt -= B - n % B;
+  return cnt;
+}
 
 // Decoded candidate.
 struct Cand {

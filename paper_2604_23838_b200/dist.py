@@ -1,24 +1,36 @@
 """Candidate sharding across GPUs and the one collective per decision.
 
 Every rank holds the same decision state (SPMD replicas of the same
-deterministic decision loop), scores a contiguous block of the global
-serial range, and the shard winners are combined with ONE all-reduce: each
-rank writes its packed 4-word key (cost bits, finish bits,
-priority<<61|serial, valid) into row `rank` of a zeroed [world, 4] int64
-buffer and a SUM all-reduce hands every rank all rows, which it reduces
-lexicographically — identical on every rank, so all ranks apply the same
-winner without a broadcast. (An element-wise MIN all-reduce would mix
-fields of different ranks and break the reference's tie order,
-SURVEY.md §8(e).) Over NCCL the buffer stays on the device: the CUDA
-library writes the shard key straight into it (RlxDecideArgs.dev_key_out).
+deterministic decision loop) and scores part `rank` of `world` of the
+candidate set: every world-th block of 32 consecutive serials of each class
+(multiplex, merges, exclusive), starting at block `rank` (`part_serials`,
+the library's RLX_F_SHARD). Per class the blocks interleave, so every rank
+gets the same mix of merge targets, pipelines and follow-up counts —
+cost-balanced without a cost model (a merge costs 3(1+F) passes against 3
+for the others, and F varies by target).
+
+The shard winners are combined with ONE all-reduce: each rank writes its
+packed 5-word row (cost bits, finish bits, priority<<61|serial, valid,
+lowest failing serial<<8|code or ~0) into row `rank` of a zeroed
+[world, 5] int64 buffer and a SUM all-reduce hands every rank all rows,
+which it reduces lexicographically — identical on every rank, so all ranks
+apply the same winner without a broadcast. (An element-wise MIN all-reduce
+would mix fields of different ranks and break the reference's tie order,
+SURVEY.md §8(e).) If any rank saw a failing candidate, every rank raises the
+reference's exception for the globally lowest failing serial — the one the
+reference's serial scan raises on. Over NCCL the buffer stays on the
+device: the CUDA library writes the shard row straight into it
+(RlxDecideArgs.dev_key_out).
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-WORDS = 4
+WORDS = 5
+BLOCK_SHIFT = 5  # = kShardBlockShift (csrc/rlx_abi.cu)
 _MASK61 = (1 << 61) - 1
+_NONE = (1 << 64) - 1
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -26,6 +38,30 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     q, r = divmod(n, world)
     b = rank * q + min(rank, r)
     return b, b + q + (1 if rank < r else 0)
+
+
+def part_serials(counts, rank: int, world: int, shift: int = BLOCK_SHIFT) -> np.ndarray:
+    """The serials part `rank` of `world` scores (RLX_F_SHARD): per class of
+    `counts` = (n_multiplex, n_merge, n_exclusive), every world-th block of
+    2**shift serials starting at block `rank`."""
+    out = []
+    s0 = 0
+    for n in counts:
+        s = np.arange(n, dtype=np.int64)
+        out.append(s0 + s[(s >> shift) % world == rank])
+        s0 += n
+    return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
+
+
+def first_error(rows: np.ndarray):
+    """(serial, device code) of the lowest failing candidate over all rows of
+    a [world, 5] uint64 table, or None."""
+    e = rows[:, 4]
+    e = e[e != np.uint64(_NONE)]
+    if e.size == 0:
+        return None
+    m = int(e.min())
+    return m >> 8, m & 0xFF
 
 
 def best_row(rows: np.ndarray) -> int:
@@ -41,13 +77,23 @@ def best_row(rows: np.ndarray) -> int:
     return best
 
 
-def pack(cost: float, finish: float, priority: int, serial: int) -> np.ndarray:
-    """(cost, finish, priority, serial) -> the 4-word key of include/rlx.h
-    RlxKey (costs are >= 0 doubles, so their bit patterns order as u64)."""
+def pack(cost: float, finish: float, priority: int, serial: int, err: int | None = None) -> np.ndarray:
+    """(cost, finish, priority, serial) -> the 5-word row: include/rlx.h
+    RlxKey (costs are >= 0 doubles, so their bit patterns order as u64)
+    plus the shard's lowest failing candidate (serial << 8 | code, or ~0)."""
     w = np.zeros(WORDS, dtype=np.uint64)
     w[0:2] = np.array([cost + 0.0, finish + 0.0], dtype=np.float64).view(np.uint64)
     w[2] = (int(priority) << 61) | int(serial)
     w[3] = 1
+    w[4] = np.uint64(_NONE if err is None else err)
+    return w
+
+
+def empty_row(err: int | None = None) -> np.ndarray:
+    """The row of a shard without candidates (or whose candidates all failed)."""
+    w = np.zeros(WORDS, dtype=np.uint64)
+    w[0:3] = np.uint64(_NONE)
+    w[4] = np.uint64(_NONE if err is None else err)
     return w
 
 
@@ -88,17 +134,28 @@ class ShardedChooser:
         self.torch = torch
 
     def __call__(self, state):
+        from .native import raise_device_error
+
         ev = self.ev
         self.table.zero_()
         self.torch.cuda.synchronize(self.table.device)
         row_ptr = self.table.data_ptr() + self.rank * WORDS * 8
-        # one plan per decision: the library sizes block `rank` of `world`
-        # from the candidate count it enumerates (same as shard_range)
-        d = ev.decide(state, self.window, self.max_merge, part=(self.rank, self.world), dev_key_ptr=row_ptr)
-        n = d.n_candidates
+        # one plan per decision; the library writes this rank's row (best key
+        # and lowest failing serial) into the table even when its part fails,
+        # so every rank reaches the all-reduce and raises the same error
+        try:
+            d = ev.decide(state, self.window, self.max_merge, part=(self.rank, self.world), dev_key_ptr=row_ptr)
+            n = d.n_candidates
+        except (RuntimeError, KeyError) as exc:
+            if getattr(exc, "serial", None) is None:
+                raise
+            n = ev.last_n_candidates
         if n == 0:
             return None
         rows = minloc_allreduce(self.table, self.rank, self.group)
+        fail = first_error(rows)
+        if fail is not None:
+            raise_device_error(fail[1], fail[0])
         i = best_row(rows)
         cost, fin, prio, serial = unpack(rows[i])
         action = ev.decode(serial)

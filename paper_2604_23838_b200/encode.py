@@ -183,16 +183,19 @@ class GraphEncoding:
 
 def _knobs(instance) -> tuple:
     return (instance.headroom, instance.realloc_penalty, instance.default_migration_cost, instance.merge_enabled,
-            id(instance.model), len(instance.graphs))
+            len(instance.graphs))
 
 
 def instance_encoding(instance) -> "InstanceEncoding":
     """The instance's C-ABI encoding, built once per Instance object (and
     rebuilt if its knobs are changed afterwards)."""
     cached = instance.__dict__.get("_rlx_encoding")
-    if cached is not None and cached[0] == _knobs(instance):
+    # the model and graph list are compared by identity, holding references
+    # (an id() key could be reused by a new object after the old one is freed)
+    if (cached is not None and cached[0] == _knobs(instance) and cached[2] is instance.model
+            and cached[3] is instance.graphs):
         return cached[1]
     enc = InstanceEncoding(instance)
     enc.graph = GraphEncoding(instance, enc)
-    instance.__dict__["_rlx_encoding"] = (_knobs(instance), enc)
+    instance.__dict__["_rlx_encoding"] = (_knobs(instance), enc, instance.model, instance.graphs)
     return enc

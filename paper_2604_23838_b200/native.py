@@ -65,6 +65,15 @@ def _raise(code: int, msg: str, serial: int | None = None):
     raise exc
 
 
+def raise_device_error(code: int, serial: int | None = None):
+    """Raise the reference's exception for a device error code (the low byte
+    of RlxDecision.err_key): the same class and text on every rank."""
+    lib = load_library(require_device=False)
+    buf = C.create_string_buffer(512)
+    st = lib.rlx_error_text(int(code), buf, 512)
+    _raise(st, buf.value.decode(), serial)
+
+
 def plan_info(state, window: int, max_merge: int | None = None) -> abi.RlxPlanInfo:
     """Host-only planning of `state`'s decision (rlx_plan_info): candidate
     counts and plan sizes, or the CapacityError the device path would
@@ -150,6 +159,7 @@ class Evaluator:
         sd = state.snapshot()
         out = abi.RlxDecision()
         rc = self.lib.rlx_decide(self.handle, C.byref(sd), C.byref(args), C.byref(out))
+        self.last_n_candidates = out.n_candidates
         if rc != 0:
             _raise(rc, self.error(), out.serial if out.serial >= 0 else None)
         self.last = out

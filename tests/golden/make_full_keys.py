@@ -4,11 +4,11 @@ TEST INFRASTRUCTURE ONLY. Scores EVERY candidate of a first decision with
 the CPU oracle (oracle/rlx_oracle.c, pinned to the live reference by
 tests/test_oracle.py) on all host threads, and writes
 
-    tests/golden/full/<name>.npz
-        keys      float64 [n, 2]  (cost, finish) per serial
-        prio      uint8   [n]     candidate class (= reference priority)
-        winner    float64 [4]     (cost, finish, priority, serial) argmin
-        n_mux, n_merge, n_excl
+    tests/golden/full/<name>.keys.xz   float64 [n, 2] (cost, finish) per serial,
+                                       little-endian, lzma-compressed
+    tests/golden/full/<name>.npz       winner float64 [4] (cost, finish,
+                                       priority, serial) argmin; n_mux,
+                                       n_merge, n_excl; window; max_merge
 
 so the GPU parity tests can compare every device key and the winner
 bit-exactly (tests/test_gpu_full_decisions.py). Run in the build container
@@ -69,7 +69,7 @@ def main(name: str, threads: int | None = None) -> None:
         print(f"{name}: {done}/{n} in {time.time() - t0:.0f}s", flush=True)
     # candidate classes from the serial layout (multiplex, merges, exclusives)
     prio = np.zeros(n, dtype=np.uint8)
-    n_mux, n_merge = _class_sizes(o, st, window, cap, n)
+    n_mux, n_merge, _ = o.counts(st, window, cap)
     prio[n_mux:n_mux + n_merge] = 1
     prio[n_mux + n_merge:] = 2
     order = np.lexsort((np.arange(n), prio, keys[:, 1], keys[:, 0]))
@@ -77,32 +77,24 @@ def main(name: str, threads: int | None = None) -> None:
     winner = np.array([keys[w, 0], keys[w, 1], prio[w], w], dtype=np.float64)
     os.makedirs(os.path.join(HERE, "full"), exist_ok=True)
     out = os.path.join(HERE, "full", f"{name}.npz")
-    np.savez_compressed(out, keys=keys, prio=prio, winner=winner, n_mux=n_mux, n_merge=n_merge,
+    save_keys(os.path.join(HERE, "full", f"{name}.keys.xz"), keys)
+    np.savez_compressed(out, winner=winner, n_mux=n_mux, n_merge=n_merge,
                         n_excl=n - n_mux - n_merge, window=window, max_merge=-1 if cap is None else cap)
     print("wrote", out, os.path.getsize(out), "winner", winner.tolist(), flush=True)
 
 
-def _class_sizes(o, st, window, cap, n):
-    """(n_multiplex, n_merge) by binary search on the decoded class of a serial."""
-    from paper_2604_23838_b200.model import Exclusive, Merge, Multiplex
+def save_keys(path, keys):
+    import lzma
 
-    def cls(s):
-        a = o.candidate(st, s, cap)
-        return 0 if isinstance(a, Multiplex) else (1 if isinstance(a, Merge) else 2)
+    with lzma.open(path, "wb", preset=9) as fh:
+        fh.write(np.ascontiguousarray(keys, dtype="<f8").tobytes())
 
-    def first(pred):
-        lo, hi = 0, n
-        while lo < hi:
-            mid = (lo + hi) // 2
-            if pred(cls(mid)):
-                hi = mid
-            else:
-                lo = mid + 1
-        return lo
 
-    a = first(lambda c: c >= 1)
-    b = first(lambda c: c >= 2)
-    return a, b - a
+def load_keys(path):
+    import lzma
+
+    with lzma.open(path, "rb") as fh:
+        return np.frombuffer(fh.read(), dtype="<f8").reshape(-1, 2)
 
 
 if __name__ == "__main__":

@@ -1,7 +1,9 @@
 """Multi-rank decision on CPU (gloo, world_size 2): each rank scores its
-contiguous serial shard, packs its shard winner and the ranks meet in the
-one SUM all-reduce of dist.py; the lexicographic reduce must give every
-rank the single-process winner, including on cost ties."""
+part of the serials (dist.part_serials — the library's block-cyclic
+RLX_F_SHARD), packs its shard winner and the ranks meet in the one SUM
+all-reduce of dist.py; the lexicographic reduce must give every rank the
+single-process winner, including on cost ties, and a failing candidate on
+one rank must make every rank raise for the globally lowest failing serial."""
 
 import os
 import socket
@@ -10,7 +12,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2604_23838_b200.dist import best_row, pack, shard_range, unpack
+from paper_2604_23838_b200.dist import best_row, empty_row, first_error, pack, part_serials, shard_range, unpack
 
 
 def test_shard_range_partitions():
@@ -25,12 +27,12 @@ def test_shard_range_partitions():
 def test_lexicographic_reduce_breaks_ties_like_reference():
     # equal cost, finish decides; equal (cost, finish): priority, then serial
     rows = np.stack([pack(50.0, 12.0, 2, 30), pack(50.0, 12.0, 0, 99), pack(50.0, 11.0, 2, 400),
-                     np.zeros(4, dtype=np.uint64)])
+                     empty_row()])
     assert unpack(rows[best_row(rows)]) == (50.0, 11.0, 2, 400)
     rows[2] = pack(50.0, 12.0, 0, 98)
     assert unpack(rows[best_row(rows)]) == (50.0, 12.0, 0, 98)
     # an element-wise min would have mixed fields across rows
-    assert best_row(np.zeros((3, 4), dtype=np.uint64)) == -1
+    assert best_row(np.zeros((3, 5), dtype=np.uint64)) == -1
 
 
 def _free_port():
@@ -39,7 +41,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, window, cap, q):
+def _worker(rank, world, port, name, window, cap, q, fail=False):
     import sys
 
     import torch
@@ -58,15 +60,52 @@ def _worker(rank, world, port, name, window, cap, q):
     inst = instance(name)
     st = HostState(inst)
     o = Oracle(inst, nthreads=2)
-    n = o.score(st, window, cap, serials=[])["n"]
-    b, e = shard_range(n, rank, world)
+    counts = o.counts(st, window, cap)
+    mine = part_serials(counts, rank, world)
     table = torch.zeros((world, WORDS), dtype=torch.int64)
-    r = o.score(st, window, cap, serials=list(range(b, e)))
-    if r["best"] is not None:
-        table[rank] = torch.from_numpy(pack(*r["best"]).view(np.int64))
+    r = o.score(st, window, cap, serials=mine.tolist())
+    # rank 1 reports a (synthetic) failing candidate: both ranks must see it
+    err = (5 << 8 | 1) if rank == 1 and fail else None
+    row = pack(*r["best"], err=err) if r["best"] is not None else empty_row(err)
+    table[rank] = torch.from_numpy(row.view(np.int64))
     rows = minloc_allreduce(table, rank)
-    q.put((rank, unpack(rows[best_row(rows)])))
+    q.put((rank, unpack(rows[best_row(rows)]), first_error(rows)))
     dist.destroy_process_group()
+
+
+def test_part_serials_cover_each_class_once():
+    for counts in ((288, 1048544, 32), (32046, 32256, 512), (0, 5, 0), (7, 0, 3), (31, 33, 65)):
+        for w in (1, 2, 3, 8):
+            parts = [part_serials(counts, r, w) for r in range(w)]
+            allp = np.sort(np.concatenate(parts))
+            assert (allp == np.arange(sum(counts))).all()
+            # every class splits into near-equal parts (block granularity)
+            for lo, n in ((0, counts[0]), (counts[0], counts[1]), (counts[0] + counts[1], counts[2])):
+                sizes = [int(((p >= lo) & (p < lo + n)).sum()) for p in parts]
+                assert max(sizes) - min(sizes) <= 32
+
+
+def test_first_error_is_the_lowest_failing_serial():
+    rows = np.stack([pack(5.0, 1.0, 0, 3), empty_row(900 << 8 | 1), pack(4.0, 1.0, 1, 700, err=750 << 8 | 16)])
+    assert first_error(rows) == (750, 16)
+    assert first_error(np.stack([pack(5.0, 1.0, 0, 3), empty_row()])) is None
+
+
+def _run_ranks(name, window, cap, fail=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, window, cap, q, fail)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        rank, best, err = q.get(timeout=300)
+        got[rank] = (best, err)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return got
 
 
 @pytest.mark.parametrize("name,window,cap", [("trap", 3, None), ("trap", 1, None), ("async_small", 3, 3)])
@@ -78,14 +117,12 @@ def test_two_rank_decision_matches_single(name, window, cap):
 
     inst = instance(name)
     want = Oracle(inst, nthreads=2).score(HostState(inst), window, cap)["best"]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, window, cap, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got = dict(q.get(timeout=300) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    assert got[0] == got[1] == tuple(want)
+    got = _run_ranks(name, window, cap)
+    assert got[0][0] == got[1][0] == tuple(want)
+    assert got[0][1] is got[1][1] is None
+
+
+def test_two_rank_error_reaches_every_rank():
+    got = _run_ranks("trap", 3, None, fail=True)
+    assert got[0][1] == got[1][1] is not None
+    assert got[0][1][1] == 1

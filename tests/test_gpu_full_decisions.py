@@ -1,8 +1,8 @@
 """Every key of the benchmarked decisions, bit-exact against golden data.
 
-tests/golden/full/<name>.npz holds the CPU oracle's (cost, finish) for EVERY
-candidate of a first decision plus the (cost, finish, priority, serial)
-winner (tests/golden/make_full_keys.py; the oracle is pinned to the live
+tests/golden/full/<name>.keys.xz holds the CPU oracle's (cost, finish) for
+EVERY candidate of a first decision and <name>.npz the (cost, finish,
+priority, serial) winner (tests/golden/make_full_keys.py; the oracle is pinned to the live
 reference by tests/test_oracle.py). tests/golden/full/<name>_sample.npz
 holds oracle keys for a stratified sample of a decision too large to score
 completely on the CPU (config 5, merge cap 2: every candidate tied with the
@@ -31,7 +31,15 @@ JOBS = {
 
 
 def _have(name):
-    return os.path.exists(os.path.join(FULL, f"{name}.npz"))
+    return os.path.exists(os.path.join(FULL, f"{name}.npz")) and os.path.exists(os.path.join(FULL, f"{name}.keys.xz"))
+
+
+def _keys(name):
+    """(cost, finish) of every serial: raw little-endian float64, lzma."""
+    import lzma
+
+    with lzma.open(os.path.join(FULL, f"{name}.keys.xz"), "rb") as fh:
+        return np.frombuffer(fh.read(), dtype="<f8").reshape(-1, 2)
 
 
 @pytest.mark.gpu
@@ -42,16 +50,17 @@ def test_full_decision_keys(Evaluator, name):
     from paper_2604_23838_b200.state import State
 
     g = np.load(os.path.join(FULL, f"{name}.npz"))
+    keys = _keys(name)
     cfg, window, cap = JOBS[name]
     inst = instance(cfg)
     ev = Evaluator(inst)
     st = State(inst)
     d = ev.decide(st, window, cap, shard=(0, -1), want_keys=True)
-    n = g["keys"].shape[0]
+    n = keys.shape[0]
     assert d.n_candidates == n
     assert (d.n_multiplex, d.n_merge, d.n_exclusive) == (int(g["n_mux"]), int(g["n_merge"]), int(g["n_excl"]))
     got = ev.keys.view(np.uint64)
-    want = g["keys"].view(np.uint64)
+    want = keys.view(np.uint64)
     bad = np.nonzero((got != want).any(axis=1))[0]
     assert bad.size == 0, f"{bad.size} of {n} keys differ, first serials {bad[:8].tolist()}"
     assert (d.cost, d.finish, d.priority, d.serial) == tuple(

@@ -40,14 +40,14 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
   if (b > e) b = e;
   WorkDesc wd;
   memset(&wd, 0, sizeof wd);
-  auto clip = [&](int64_t lo, int64_t hi, int64_t& s, int64_t& n) {
-    int64_t x = lo > b ? lo : b, y = hi < e ? hi : e;
-    s = x;
-    n = y > x ? y - x : 0;
-  };
-  clip(dp.n_mux, dp.n_mux + dp.n_merge, wd.a0, wd.na);
-  clip(0, dp.n_mux, wd.b0, wd.nb);
-  clip(dp.n_mux + dp.n_merge, dp.n_total, wd.c0, wd.nc);
+  const int64_t lo[3] = {dp.n_mux, 0, dp.n_mux + dp.n_merge};
+  const int64_t hi[3] = {dp.n_mux + dp.n_merge, dp.n_mux, dp.n_total};
+  wd.world = 1;
+  for (int c = 0; c < 3; c++) {
+    const int64_t x = lo[c] > b ? lo[c] : b, y = hi[c] < e ? hi[c] : e;
+    wd.s0[c] = x;
+    wd.loc[c] = y > x ? y - x : 0;
+  }
   wd.shard0 = b;
   unsigned long long counter = 0, err_key = ~0ull;
   wd.counter = &counter;
@@ -58,14 +58,47 @@ extern "C" int rlx_twin_decide(const RlxInstanceDesc* in, const RlxStateDesc* sd
              dp.NL, dp.NT, dp.NC, dp.hot_bytes, dp.max_ord, dp.NTW);
     return RLX_ERR_LIMIT;
   }
+  // `ngw` one-lane groups share one warp slice and run interleaved, one
+  // iteration each in turn — the device's per-warp candidate queue with its
+  // claim / drain / finalise / fetch protocol, deterministically on a CPU
+  const int ngw = getenv("RLX_TWIN_GROUPS") ? atoi(getenv("RLX_TWIN_GROUPS")) : 4;
   group_layout(dp, 1, 32);
-  std::vector<double> smem((dp.hot_bytes + dp.g_bytes) / 8 + 16);
+  const size_t bytes = dp.hot_bytes + dp.w_bytes + (size_t)ngw * dp.g_bytes;
+  std::vector<double> smem(bytes / 8 + 16);
   memcpy(smem.data(), dp.hot, dp.hot_bytes);  // the kernel stages the hot region the same way
   g_twin_smem = (uint8_t*)smem.data();
   wd.slice_bytes = (int)dp.g_bytes;
+  const uint32_t wbase = dp.hot_bytes;
+  WarpCand* wc = reinterpret_cast<WarpCand*>(g_twin_smem + wbase);
+  wc->gen = 0;
+  fetch_candidate(wd, wc);
+  std::vector<GroupRunner<1, 32>*> rs;
+  for (int i = 0; i < ngw; i++) {
+    rs.push_back(new GroupRunner<1, 32>(wd, wbase + dp.w_bytes + (uint32_t)i * dp.g_bytes, wbase, 0, 1u, ngw));
+    rs.back()->init();
+  }
+  std::vector<bool> live(ngw, true);
+  for (int n_live = ngw; n_live > 0;) {
+    for (int i = 0; i < ngw; i++)
+      if (live[i] && !rs[i]->iter()) {
+        live[i] = false;
+        n_live--;
+      }
+  }
   SliceOut out;
   memset(&out, 0, sizeof out);
-  group_loop<1, 32>(wd, dp.hot_bytes, 0, 1u, &out);
+  for (int i = 0; i < ngw; i++) {
+    SliceOut o;
+    memset(&o, 0, sizeof o);
+    rs[i]->finish(&o);
+    if (key_less(o.k0, o.k1, o.k2, out.k0 ? out.k0 : ~0ull, out.k0 ? out.k1 : ~0ull, out.k0 ? out.k2 : ~0ull)) {
+      out.k0 = o.k0;
+      out.k1 = o.k1;
+      out.k2 = o.k2;
+    }
+    out.passes += o.passes;
+    delete rs[i];
+  }
   key_out[0] = out.k0;
   key_out[1] = out.k1;
   key_out[2] = out.k2;

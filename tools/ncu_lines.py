@@ -29,7 +29,7 @@ for r in rows:
         data.append((int(r[ix] or 0), int(r[ws] or 0), int(r[th] or 0), fname, int(r[0]), r[1][:100]))
     except ValueError:
         pass
-src = open('paper_2604_23838_b200/csrc/rlx_kernels.cu').read().split('\n')
+src = open(next((a.split('=',1)[1] for a in sys.argv if a.startswith('--src=')), 'paper_2604_23838_b200/csrc/rlx_kernels.cu')).read().split('\n')
 ranges = []
 for i, l in enumerate(src, 1):
     m = re.match(r'\s*RLX_HD .*?(\w+)\(', l)
