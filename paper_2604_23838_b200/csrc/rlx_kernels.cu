@@ -384,10 +384,25 @@ struct Lane {
     return reinterpret_cast<const T*>(SMEM + off);
   }
   // ---- hot plan (shared memory)
-  RLX_HD int hkind(int n) const { return arr<uint8_t>(PLAN.o_kind)[n]; }
-  RLX_HD int hpipe(int n) const { return arr<uint8_t>(PLAN.o_pipe)[n]; }
-  RLX_HD int hworker(int n) const { return arr<uint16_t>(PLAN.o_worker)[n]; }
-  RLX_HD int hflags(int n) const { return arr<uint8_t>(PLAN.o_flags)[n]; }
+  RLX_HD NodeRec rec(int n) const {  // one 16-byte shared load
+#ifdef __CUDA_ARCH__
+    const uint4 v = arr<uint4>(PLAN.o_rec)[n];
+    return NodeRec{v.x, v.y, v.z, v.w};
+#else
+    return arr<NodeRec>(PLAN.o_rec)[n];
+#endif
+  }
+  RLX_HD uint32_t recw(int n, int k) const { return arr<uint32_t>(PLAN.o_rec)[4 * n + k]; }
+  RLX_HD int hkind(int n) const { return (int)(recw(n, 2) >> 24); }
+  RLX_HD int hpipe(int n) const { return (int)(recw(n, 3) & 0xFF); }
+  RLX_HD int hworker(int n) const { return (int)(recw(n, 2) & 0xFFFF); }
+  static RLX_HD int r_worker(const NodeRec& r) { return (int)(r.z & 0xFFFF); }
+  static RLX_HD int r_flags(const NodeRec& r) { return (int)((r.z >> 16) & 0xFF); }
+  RLX_HD int r_pos(const NodeRec& r) const {  // position in this pass's order (merge-shifted)
+    int p = (int)((r.w >> (o ? 16 : 8)) & 0xFF);
+    if (r_worker(r) == mt && p >= ins) p++;
+    return p;
+  }
   RLX_HD double hdur(int n) const { return arr<double>(PLAN.o_dur)[n]; }
   RLX_HD double hmem(int n) const { return arr<double>(PLAN.o_mem)[n]; }
   RLX_HD double hmpre(int n) const { return arr<double>(PLAN.o_mprefix)[n]; }
@@ -412,48 +427,47 @@ struct Lane {
     }
     return arr<uint16_t>(PLAN.o_ord)[(o * PLAN.W + w) * kMaxPos + p];
   }
-  RLX_HD int pos_of(int n) const {
-    int p = arr<uint8_t>(PLAN.o_pos)[o * PLAN.NL + n];
-    if (hworker(n) == mt && p >= ins) p++;
-    return p;
-  }
+  RLX_HD int pos_of(int n) const { return r_pos(rec(n)); }
 
   // ---- completion bookkeeping (succs of a completed node; readiness)
-  RLX_HD void became_ready(int s) {
-    const int f = hflags(s);
+  RLX_HD void became_ready(int s, const NodeRec& r) {
+    const int f = r_flags(r);
     if (f & F_TW) {
       const int q = at_add<G>(&gc()->twq_n, 1);
       twq()[q] = (uint16_t)s;
     } else if (f & F_WIN) {
-      at_or_bit<G>(&mask()[hworker(s)], pos_of(s));
+      at_or_bit<G>(&mask()[r_worker(r)], r_pos(r));
     }
   }
-  RLX_HD void fire(int s) {
-    if (hflags(s) & F_JOIN) {  // a join releases its members, whose only predecessor it is
-      const int32_t* so = arr<int32_t>(PLAN.o_succ_off);
+  RLX_HD void fire(int s, const NodeRec& r) {
+    if (r_flags(r) & F_JOIN) {  // a join releases its members, whose only predecessor it is
       const uint16_t* sl = arr<uint16_t>(PLAN.o_succ);
-      for (int e = so[s], e1 = so[s + 1]; e < e1; e++) became_ready(sl[e]);
+      for (uint32_t e = r.x, e1 = r.x + (r.y & 0xFFFF); e < e1; e++) {
+        const int t = sl[e];
+        became_ready(t, rec(t));
+      }
     } else {
-      became_ready(s);
+      became_ready(s, r);
     }
   }
   RLX_HD void dec(int s) {
-    const unsigned c = arr<uint16_t>(PLAN.o_ctr_idx)[s];
-    if (c == 0xFFFFu || at_sub<G>(&ctr()[c], 1u) == 1u) fire(s);
+    const NodeRec r = rec(s);
+    const unsigned c = r.y >> 16;
+    if (c == 0xFFFFu || at_sub<G>(&ctr()[c], 1u) == 1u) fire(s, r);
   }
-  RLX_HD void succs_of(int u) {
-    const int32_t* so = arr<int32_t>(PLAN.o_succ_off);
+  RLX_HD void succs_of(const NodeRec& r) {
     const uint16_t* sl = arr<uint16_t>(PLAN.o_succ);
-    for (int e = so[u], e1 = so[u + 1]; e < e1; e++) dec(sl[e]);
+    for (uint32_t e = r.x, e1 = r.x + (r.y & 0xFFFF); e < e1; e++) dec(sl[e]);
   }
   RLX_HD void complete(int n, unsigned& ld) {
     if (n == PLAN.M) {
       ld++;
       const WarpCand* c = wc();
-      for (int i = 0; i < c->k; i++) succs_of(c->m[i]);
+      for (int i = 0; i < c->k; i++) succs_of(rec(c->m[i]));
     } else {
-      if (hflags(n) & F_WIN) ld++;
-      succs_of(n);
+      const NodeRec r = rec(n);
+      if (r_flags(r) & F_WIN) ld++;
+      succs_of(r);
     }
   }
 
@@ -469,7 +483,7 @@ struct Lane {
       *g = am;
     }
     const double d = dur(n);
-    const double rinv = recip(rate);
+    const double rinv = rate == 1.0 ? 1.0 : recip(rate);  // exclusive starts run at 1.0 (slowdown.py:94-99)
 #pragma unroll
     for (int jj = 0; jj < WPL; jj++) {  // predicated register select (no per-lane branches)
       const bool hit = jj == j;
@@ -618,17 +632,20 @@ struct Lane {
   // ---- selection on idle workers (one sweep)
   RLX_HD void select(bool pair) {
     const int W = PLAN.W;
+    unsigned long long* mk = mask();
+    // idle local workers with a ready node: the masks load in parallel, the
+    // loop below visits only workers that start something
     unsigned idle = 0;
 #pragma unroll
-    for (int j = 0; j < WPL; j++)
-      if (lane + G * j < W && !((rb >> (2 * j)) & Bits(3))) idle |= 1u << j;
-    unsigned long long* mk = mask();
+    for (int j = 0; j < WPL; j++) {
+      const int w = lane + G * j;
+      if (w < W && !((rb >> (2 * j)) & Bits(3)) && mk[w] != 0ull) idle |= 1u << j;
+    }
     while (idle) {
       const int j = ffs32(idle) - 1;
       idle &= idle - 1;
       const int w = lane + G * j;
       unsigned long long m = mk[w];
-      if (!m) continue;
       const int p = ffs64(m) - 1;
       const int x = node_at(w, p);
       int first = x, second = -1, al = 0;
@@ -642,9 +659,8 @@ struct Lane {
           if (pipe(y) != px) {
             if (x != PLAN.M && y != PLAN.M) {  // decision-invariant pair: planner table
               const int cnt = arr<uint8_t>(PLAN.o_ord_cnt)[w];
-              const uint8_t* po = arr<uint8_t>(PLAN.o_pos) + PLAN.NL;  // name-order positions
-              const int ent =
-                  arr<uint8_t>(PLAN.o_ptab)[arr<uint32_t>(PLAN.o_pt_off)[w] + po[x] * cnt + po[y]];
+              const int ent = arr<uint8_t>(PLAN.o_ptab)[arr<uint32_t>(PLAN.o_pt_off)[w] +
+                                                        ((recw(x, 3) >> 16) & 0xFF) * cnt + ((recw(y, 3) >> 16) & 0xFF)];
               if (ent >= 0x60 && ent < 0x80) {
                 if (err < kErrKeyBase)  // the first LUT lookup of _best_pair_action that misses
                   err = (ent & 1) ? key_err(hkind(y), hkind(x)) : key_err(hkind(x), hkind(y));
@@ -686,17 +702,20 @@ struct Lane {
     const bool dpos = dt > kEps;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
+      double fe[2];
 #pragma unroll
       for (int s = 0; s < 2; s++) {
         const Bits bit = Bits(1) << (2 * j + s);
+        fe[s] = INFINITY;
         // slot 1 (the second member of a pair) is rare: branch on it; slot 0
         // is evaluated branch-free and masked
         if (s == 1 && !(rb & bit)) continue;
         const bool on = (rb & bit) != Bits(0);
         double d = dt;
         double p = 0.0;
+        double base = now;  // now + prefix_left (:328); prefix 0 on the common path
         bool dp = dpos;
-        if (pm & bit) {
+        if (pm & bit) {  // pending merge prefix / realloc penalty (:330-333)
           p = pr[2 * j + s];
           if (p > kEps) {
             const double used = d < p ? d : p;
@@ -705,6 +724,7 @@ struct Lane {
             pr[2 * j + s] = p;
             dp = d > kEps;
           }
+          base = now + p;
         }
         double wv = wk[j][s];
         const double r = rt[j][s];
@@ -716,7 +736,10 @@ struct Lane {
         const double nw = z > 0.0 ? z : 0.0;
         wv = (on && dp && wv > kEps) ? nw : wv;
         wk[j][s] = wv;
-        if (on && p <= kEps && wv * r <= kEps) fb |= bit;
+        const double prod = wv * r;  // shared by the finish test (:604-608) and the estimate (:328)
+        const bool fin = on && p <= kEps && prod <= kEps;
+        if (fin) fb |= bit;
+        fe[s] = (on && !fin) ? base + prod : INFINITY;
       }
       const Bits both = Bits(3) << (2 * j);
       if ((fb & both) && (rb & both) != (fb & both)) {
@@ -728,17 +751,13 @@ struct Lane {
             rt[j][s] = 1.0;
             ri[j][s] = 1.0;
             pf &= ~bit;
+            const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
+            fe[s] = ((pm & bit) ? now + p : now) + wk[j][s] * 1.0;
           }
         }
       }
-#pragma unroll
-      for (int s = 0; s < 2; s++) {  // next finish estimates of the survivors (:328)
-        const Bits bit = Bits(1) << (2 * j + s);
-        if (s == 1 && !(rb & bit)) continue;
-        const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
-        const double fe = (now + p) + wk[j][s] * rt[j][s];
-        tl = ((rb & bit) && !(fb & bit) && fe < tl) ? fe : tl;
-      }
+      tl = fe[0] < tl ? fe[0] : tl;
+      tl = fe[1] < tl ? fe[1] : tl;
     }
     rb &= ~fb;
     const int* nd = nds();
@@ -1278,7 +1297,10 @@ __device__ __forceinline__ void stage_hot(uint8_t* dst, const uint8_t* src, uint
 #ifndef RLX_T2
 #define RLX_T2 512
 #endif
-constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : WPL <= 2 ? RLX_T2 : 512; }
+#ifndef RLX_T4
+#define RLX_T4 512
+#endif
+constexpr int threads_for(int WPL) { return WPL >= 8 ? RLX_T8 : WPL <= 2 ? RLX_T2 : RLX_T4; }
 
 #ifndef RLX_MINB2
 #define RLX_MINB2 1

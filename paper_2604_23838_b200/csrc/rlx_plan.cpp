@@ -530,6 +530,19 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   for (int w = 0; w < W; w++) max_ord = std::max(max_ord, (int)ordcnt[w]);
   d.max_ord = max_ord;
 
+  // ---- packed node records (hot): one 16-byte load per node on the device
+  std::vector<NodeRec> rec(NT);
+  for (int u = 0; u < NT; u++) {
+    NodeRec& r = rec[u];
+    r.x = (uint32_t)soff[u];
+    r.y = (uint32_t)(soff[u + 1] - soff[u]) | (uint32_t)ctr_idx[u] << 16;
+    const bool node = u < NL;
+    r.z = (node ? (uint32_t)worker[u] : 0u) | (uint32_t)flags[u] << 16 | (node ? (uint32_t)kind[u] : 0u) << 24;
+    r.w = (node ? (uint32_t)pipe[u] : 0u) | (uint32_t)(node ? pos[u] : 255) << 8 | (uint32_t)(node ? pos[NL + u] : 255) << 16;
+  }
+  for (int u = 0; u < NT; u++)
+    if (soff[u + 1] - soff[u] > 0xFFFF) { err = "a node with more than 65535 successors"; return RLX_ERR_LIMIT; }
+
   // ---- blob: the hot region (staged into shared memory) comes first
   Blob& B = hp.blob;
   B.buf.clear();
@@ -539,22 +552,24 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.dur = B.putv(dur);
   L.mem = B.putv(mem);
   L.mprefix = B.putv(mpre);
-  L.succ_off = B.putv(soff);
+  L.rec = B.putv(rec);
   L.ord = B.putv(ord);
-  L.kind = B.putv(kind);
-  L.pipe = B.putv(pipe);
-  L.worker = B.putv(worker);
-  L.flags = B.putv(flags);
-  L.pos = B.putv(pos);
   L.tw_slot = B.putv(twslot);
   L.tw_node = B.putv(twnode);
-  L.ctr_idx = B.putv(ctr_idx);
   L.pt_off = B.putv(pt_off);
   L.ord_cnt = B.putv(ordcnt);
   L.ptab = B.putv(ptab);
   L.succ = B.putv(sl);
   L.hot_end = (B.buf.size() + 15) & ~size_t(15);
   B.buf.resize(L.hot_end);
+  // cold copies for the candidate prologues (global loads)
+  L.succ_off = B.putv(soff);
+  L.kind = B.putv(kind);
+  L.pipe = B.putv(pipe);
+  L.worker = B.putv(worker);
+  L.flags = B.putv(flags);
+  L.pos = B.putv(pos);
+  L.ctr_idx = B.putv(ctr_idx);
   L.ctr0 = B.putv(ctr0);
   L.suffix = B.putv(lsuf);
   L.msx = B.putv(lmsx);
@@ -591,7 +606,6 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   return RLX_OK;
 }
 
-// Serial block `r` of `w` (RLX_F_SHARD): contiguous, sizes differ by <= 1.
 // The device path's capacity checks that depend only on the plan: a kernel
 // shape for W workers and the shared-memory footprint of the hot region.
 int check_capacity(const HostPlan& hp, std::string& err) {
@@ -669,14 +683,8 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.ctr0 = at<uint16_t>(base, L.ctr0);
   d.hot = base;
   d.hot_bytes = (uint32_t)L.hot_end;
-  d.o_kind = (uint32_t)L.kind;
-  d.o_pipe = (uint32_t)L.pipe;
-  d.o_worker = (uint32_t)L.worker;
-  d.o_flags = (uint32_t)L.flags;
-  d.o_pos = (uint32_t)L.pos;
+  d.o_rec = (uint32_t)L.rec;
   d.o_tw_slot = (uint32_t)L.tw_slot;
-  d.o_ctr_idx = (uint32_t)L.ctr_idx;
-  d.o_succ_off = (uint32_t)L.succ_off;
   d.o_succ = (uint32_t)L.succ;
   d.o_ord = (uint32_t)L.ord;
   d.o_dur = (uint32_t)L.dur;

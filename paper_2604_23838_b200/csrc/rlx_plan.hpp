@@ -41,6 +41,15 @@ constexpr uint8_t F_JOIN = 4;      // join counter
 constexpr uint8_t F_READY0 = 8;    // ready at the decision state
 constexpr uint8_t F_RUN0 = 16;     // running at the decision state
 
+// Packed per-node record of the hot region: everything the completion and
+// selection paths read about a node in one 16-byte shared-memory load.
+//   x: successor CSR offset        y: successor count | counter slot << 16 (0xFFFF: none)
+//   z: worker | flags << 16 | kind << 24
+//   w: pipeline | position in the suffix-key order << 8 | in the name-key order << 16 (255: none)
+struct NodeRec {
+  uint32_t x, y, z, w;
+};
+
 struct MergeBlock {
   int64_t serial0;   // first serial of the block
   int64_t combos;    // valid combos (each has `size` targets)
@@ -70,8 +79,8 @@ struct DevPlan {
   // copies and addresses it through these byte offsets.
   const uint8_t* hot;
   uint32_t hot_bytes;
-  uint32_t o_kind, o_pipe, o_worker, o_flags, o_pos, o_tw_slot, o_ctr_idx, o_succ_off, o_succ, o_ord, o_dur,
-      o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab, o_ord_cnt;
+  uint32_t o_rec, o_tw_slot, o_succ, o_ord, o_dur, o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab,
+      o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
   uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
   uint32_t w_bytes;  // warp slice (one candidate and its pass queue)
