@@ -1003,6 +1003,19 @@ RLX_HD void build_passes(WarpCand* c) {
   c->total = c->cerr ? 0 : n * c->n_var;
 }
 
+// Pass index -> (action, variant). Default: variant-major, so the groups of
+// a warp run the same variant of sibling actions at the same time;
+// RLX_PASS_ORDER=1 (tuning) runs the variants of one action together.
+RLX_HD void split_pass(int q, int na, int nv, int& a, int& v) {
+  if (PLAN.pass_order) {
+    a = q / nv;
+    v = q % nv;
+  } else {
+    a = q % na;
+    v = q / na;
+  }
+}
+
 // The action of action index `ai` of the warp's candidate.
 RLX_HD Act pass_action(const WarpCand* c, int ai) {
   if (c->cls != 1) return Act{c->cls, c->a, c->b, c->alloc};
@@ -1212,8 +1225,9 @@ struct GroupRunner {
             }
             break;
           }
-          const int na = c->n_act;
-          const int ri = (t % na) * 3 + t / na;  // reference order: action-major, variant-minor
+          int ta, tv;
+          split_pass(t, c->n_act, c->n_var, ta, tv);
+          const int ri = ta * 3 + tv;  // reference order: action-major, variant-minor
           if ((ri << 8) > c->err) continue;  // an earlier pass of this candidate already failed
           q = t;
           st = 0;
@@ -1226,9 +1240,8 @@ struct GroupRunner {
     if (st == 1) return true;
     q = (int)gbcast<G>(S.gm, q);
     fence_block();
-    const int na = c->n_act;
-    const int ai = q % na;
-    variant = q / na;
+    int ai;
+    split_pass(q, c->n_act, c->n_var, ai, variant);
     ref_idx = ai * 3 + variant;
     pair = variant == 1;
     nwin = c->nwin;
@@ -1394,10 +1407,12 @@ typedef void (*KernelFn)(const WorkDesc, SliceOut*);
 // registers, G = the smallest power of two with G * WPL >= W. RLX_SHAPE=G,WPL
 // overrides it (tuning).
 void choose_shape(int W, int& G, int& WPL) {
-  // measured (profiles/r01_shape_sweep*.txt): 2 workers/lane up to 16
-  // workers (config 2: 8x2 1.01 s vs 4x4 1.20 s), 4 above (config 3: 8x4
-  // 3.56 s vs 16x2 4.25 s); 8+ workers/lane lose occupancy.
-  WPL = W <= 16 ? 2 : 4;
+  // measured with the per-warp pass queue (profiles/r02_shape_sweep.txt):
+  // config 2 (16 workers) 4x4 874 ms vs 8x2 917 ms vs 2x8 1250 ms; config 5
+  // (64 workers) 16x4 6.35 s vs 8x8 7.87 s vs 32x2 8.18 s. Four workers per
+  // lane, as few lanes per group as cover W: more groups share a warp and
+  // drain one candidate's near-identical passes together.
+  WPL = W <= 8 ? 2 : 4;
   G = 1;
   while (G * WPL < W) G *= 2;
 }
@@ -1454,6 +1469,7 @@ int launch_score(const DevPlan& P, WorkDesc wd, SliceOut* outs, int max_slices, 
   if (!fn || G * WPL < P.W) return RLX_ERR_LIMIT;
   DevPlan P2 = P;
   group_layout(P2, G, WPL);
+  P2.pass_order = getenv("RLX_PASS_ORDER") ? atoi(getenv("RLX_PASS_ORDER")) : 0;  // tuning
   const size_t gb = P2.g_bytes, wb = P2.w_bytes;
   wd.slice_bytes = (int)gb;
   const size_t hot = P.hot_bytes;

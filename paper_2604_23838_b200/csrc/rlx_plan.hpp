@@ -73,6 +73,7 @@ struct DevPlan {
   int32_t max_ord;  // longest per-worker order (ready-mask width)
   int32_t same_order;  // 1: suffix order == name order on every worker
   int32_t acts_cap;  // merge follow-up list capacity per warp slice (set at launch)
+  int32_t pass_order;  // 0: variant-major pass queue (default), 1: action-major (tuning; set at launch)
 
   // Hot region: the leading `hot_bytes` of the plan blob hold every array the
   // event loop touches; the kernel stages it into shared memory with TMA bulk
