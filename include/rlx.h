@@ -345,6 +345,85 @@ typedef struct RlxPlanInfo {
 int rlx_plan_info(const RlxInstanceDesc* inst, const RlxStateDesc* state, int32_t window, int32_t max_merge,
                   RlxPlanInfo* out, char* err, int32_t err_len);
 
+/* ---- Sub-Stage Graph construction from rollout length tables ---------- */
+
+/* One pipeline's sample batch (rlmux PipelineSpec.samples, workload.py:59-110):
+ * per sample its prompt and turns (prefill tokens injected at the turn,
+ * decode tokens, tool latency after the turn); samples are assigned to
+ * workers round-robin (workload.py round_robin_assignment) unless
+ * `worker_of` is given. Replaces expand_to_trace + construct_graph's
+ * rollout part (workload.py:275-392, graph.py:206-362). */
+typedef struct RlxRolloutTables {
+  int32_t n_samples;
+  int32_t n_workers;             /* dp workers                                            */
+  const int32_t* worker_of;      /* [n_samples] or NULL (sample i -> worker i % n_workers) */
+  const int64_t* prompt;         /* [n_samples]                                           */
+  const int32_t* turn_off;       /* [n_samples + 1] CSR into the turn arrays              */
+  const int64_t* turn_prefill;   /* [n_turns]                                             */
+  const int64_t* turn_decode;    /* [n_turns]                                             */
+  const double* turn_tool;       /* [n_turns] tool latency after the turn (0: none)       */
+  double latency[5];             /* per-step latency: buckets 0..2, reference, training   */
+} RlxRolloutTables;
+
+/* One rollout sub-stage: worker `worker`, sequence `seq` (id
+ * "<pipeline>/w<worker>/r<seq:03d>"), in worker order then sequence order. */
+typedef struct RlxSegment {
+  int32_t worker, seq;
+  int32_t kind;                  /* RLX_KIND_* (PrefillBurst / Decode* / ToolWait)        */
+  int32_t bucket;                /* stable token bucket, -1 for a tool wait               */
+  int64_t step_lo, step_hi;      /* step_span                                             */
+  int64_t decode;                /* remaining_decode_tokens                               */
+  int64_t active0;               /* active_requests (first step)                          */
+  int64_t context0;              /* context_tokens (first step; 0 for a tool wait)        */
+  int64_t tokens;                /* token_total                                           */
+  double duration;               /* steps x latency[bucket] (tool wait: x latency[0])     */
+} RlxSegment;
+
+/* Replay every (pipeline, worker) cohort and segment its step records on
+ * `device` (stability window L_s = `window`, bucket lower bounds
+ * `bucket_bounds[0..n_buckets)` starting at 0, n_buckets <= 5). The result
+ * handle holds each pipeline's segments (rlx_graph_segments). */
+int rlx_graph_build(int device, int32_t n_pipes, const RlxRolloutTables* tables, const int32_t* bucket_bounds,
+                    int32_t n_buckets, int32_t window, void** result);
+int rlx_graph_segments(void* result, int32_t pipe, RlxSegment* out, int64_t cap, int64_t* n_out);
+int rlx_graph_stats(void* result, double* kernel_ms, int64_t* n_records);
+const char* rlx_graph_error(void* result);
+void rlx_graph_free(void* result);
+
+/* ---- batched replay of schedules into metrics (rlmux/sim.py:69-173) ---- */
+
+/* One timed action of a schedule: node ids are NUL-terminated strings in a
+ * shared blob (`n_ids` consecutive ones from `id_off`: Exclusive 1,
+ * Multiplex 2, Merge the members); `sm`/`mem` the allocation of node a;
+ * `target_worker` the Merge target (external worker id). */
+typedef struct RlxSimAction {
+  double start;
+  double sm, mem;
+  int32_t cls;                   /* RLX_CLASS_*                                           */
+  int32_t target_worker;
+  int32_t n_ids;
+  int32_t id_off;
+} RlxSimAction;
+
+typedef struct RlxSimResult {
+  int32_t status;                /* RLX_OK, or the status simulate() raises with          */
+  int32_t action_index;          /* failing action (n: the final drain), -1 if none       */
+  double makespan;
+  double throughput;             /* aggregate_throughput                                  */
+  int64_t total_tokens;
+  char error[192];               /* the reference's message                               */
+} RlxSimResult;
+
+/* Replay schedules [s] = actions [sched_off[s], sched_off[s+1]) on copies of
+ * the instance's initial ExecState, over `n_threads` host threads (<= 0: all).
+ * Outputs per schedule: result, per-pipeline latency / tokens [n_sched * P]
+ * (pipelines in instance order) and per-worker average utilisation
+ * [n_sched * W] (dense worker order). Allocations must be in the instance's
+ * LUT (RLX_ERR_LIMIT otherwise). */
+int rlx_simulate_batch(const RlxInstanceDesc* inst, const RlxGraphDesc* graph, int32_t n_sched,
+                       const int64_t* sched_off, const RlxSimAction* actions, const char* ids, int32_t n_threads,
+                       RlxSimResult* results, double* pipe_latency, int64_t* pipe_tokens, double* util_avg);
+
 int rlx_abi_version(void);
 int rlx_open(int device, void** handle);
 int rlx_load_instance(void* handle, const RlxInstanceDesc* inst);

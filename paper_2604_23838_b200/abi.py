@@ -144,12 +144,36 @@ class RlxPlanInfo(C.Structure):
                 ("max_worker_order", C.c_int32), ("hot_bytes", C.c_int32), ("blob_bytes", C.c_int64)]
 
 
+class RlxRolloutTables(C.Structure):
+    _fields_ = [("n_samples", C.c_int32), ("n_workers", C.c_int32), ("worker_of", C.POINTER(C.c_int32)),
+                ("prompt", C.POINTER(C.c_int64)), ("turn_off", C.POINTER(C.c_int32)),
+                ("turn_prefill", C.POINTER(C.c_int64)), ("turn_decode", C.POINTER(C.c_int64)),
+                ("turn_tool", C.POINTER(C.c_double)), ("latency", C.c_double * 5)]
+
+
+class RlxSegment(C.Structure):
+    _fields_ = [("worker", C.c_int32), ("seq", C.c_int32), ("kind", C.c_int32), ("bucket", C.c_int32),
+                ("step_lo", C.c_int64), ("step_hi", C.c_int64), ("decode", C.c_int64), ("active0", C.c_int64),
+                ("context0", C.c_int64), ("tokens", C.c_int64), ("duration", C.c_double)]
+
+
+class RlxSimAction(C.Structure):
+    _fields_ = [("start", C.c_double), ("sm", C.c_double), ("mem", C.c_double), ("cls", C.c_int32),
+                ("target_worker", C.c_int32), ("n_ids", C.c_int32), ("id_off", C.c_int32)]
+
+
+class RlxSimResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("action_index", C.c_int32), ("makespan", C.c_double),
+                ("throughput", C.c_double), ("total_tokens", C.c_int64), ("error", C.c_char * 192)]
+
+
 # Every symbol include/rlx.h declares (checked by tests/test_abi.py).
 EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "rlx_decode",
             "rlx_last_error", "rlx_error_text", "rlx_close", "rlx_set_stream", "rlx_drive", "rlx_plan_info",
             "rlx_state_create", "rlx_state_clone", "rlx_state_destroy", "rlx_state_error", "rlx_state_apply",
             "rlx_state_advance", "rlx_state_info", "rlx_state_snapshot", "rlx_state_node", "rlx_state_events",
-            "rlx_state_completion")
+            "rlx_state_completion", "rlx_graph_build", "rlx_graph_segments", "rlx_graph_stats", "rlx_graph_error",
+            "rlx_graph_free", "rlx_simulate_batch")
 
 
 def bind(lib: C.CDLL) -> C.CDLL:
@@ -199,6 +223,22 @@ def bind(lib: C.CDLL) -> C.CDLL:
     lib.rlx_state_node.argtypes = [C.c_void_p, C.c_int32, C.POINTER(RlxNodeInfo)]
     lib.rlx_state_events.restype = C.c_int
     lib.rlx_state_events.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(RlxEvent)]
+    lib.rlx_graph_build.restype = C.c_int
+    lib.rlx_graph_build.argtypes = [C.c_int, C.c_int32, C.POINTER(RlxRolloutTables), C.POINTER(C.c_int32), C.c_int32,
+                                    C.c_int32, C.POINTER(C.c_void_p)]
+    lib.rlx_graph_segments.restype = C.c_int
+    lib.rlx_graph_segments.argtypes = [C.c_void_p, C.c_int32, C.POINTER(RlxSegment), C.c_int64, C.POINTER(C.c_int64)]
+    lib.rlx_graph_stats.restype = C.c_int
+    lib.rlx_graph_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    lib.rlx_graph_error.restype = C.c_char_p
+    lib.rlx_graph_error.argtypes = [C.c_void_p]
+    lib.rlx_graph_free.restype = None
+    lib.rlx_graph_free.argtypes = [C.c_void_p]
+    lib.rlx_simulate_batch.restype = C.c_int
+    lib.rlx_simulate_batch.argtypes = [C.POINTER(RlxInstanceDesc), C.POINTER(RlxGraphDesc), C.c_int32,
+                                       C.POINTER(C.c_int64), C.POINTER(RlxSimAction), C.c_char_p, C.c_int32,
+                                       C.POINTER(RlxSimResult), C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double)]
     lib.rlx_state_completion.restype = C.c_int
     lib.rlx_state_completion.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_double)]
     return lib

@@ -140,3 +140,83 @@ def simulate(schedule, instance) -> SimulationReport:
                             per_pipeline_tokens=tokens, aggregate_throughput=total / makespan if makespan > 0 else 0.0,
                             utilization_avg=util_avg, utilization_series=util_series, events=events,
                             policy=schedule.policy, metadata=dict(schedule.metadata))
+
+
+def simulate_batch(schedules, instance, threads: int | None = None) -> list:
+    """`simulate` for many schedules of one instance:
+    every schedule is replayed on its own copy of the native ExecState in
+    librlx.so (csrc/rlx_sim.cpp), over `threads` host threads (default: all),
+    with the metrics folded natively in the reference's operation order.
+    The reports equal `simulate`'s field for field except `events` and
+    `utilization_series`, which stay empty (the batch keeps only the
+    averages). A schedule whose allocations fall outside the instance's
+    slowdown LUT is replayed by `simulate` instead. The first failing
+    schedule raises the exception `simulate` would raise for it."""
+    import ctypes as C
+
+    from . import abi
+    from .encode import instance_encoding
+    from .model import Exclusive, Multiplex
+    from .native import load_library
+
+    inst = as_instance(instance)
+    enc = instance_encoding(inst)
+    lib = load_library(require_device=False)
+    scheds = list(schedules)
+    acts, blob, off = [], bytearray(), [0]
+    for sched in scheds:
+        for timed in sched.actions:
+            a = action_from(timed.action)
+            x = abi.RlxSimAction()
+            x.start = float(timed.start)
+            if isinstance(a, Exclusive):
+                ids = [a.node_id]
+                x.cls, x.sm, x.mem = abi.CLASS_EXCLUSIVE, a.alloc.sm_share, a.alloc.mem_share
+            elif isinstance(a, Multiplex):
+                ids = [a.node_a, a.node_b]
+                x.cls, x.sm, x.mem = abi.CLASS_MULTIPLEX, a.alloc_a.sm_share, a.alloc_a.mem_share
+            else:
+                ids = list(a.member_ids)
+                x.cls, x.target_worker = abi.CLASS_MERGE, int(a.target_worker)
+            x.n_ids, x.id_off = len(ids), len(blob)
+            for nid in ids:
+                blob += nid.encode() + b"\0"
+            acts.append(x)
+        off.append(len(acts))
+    n = len(scheds)
+    P, W = len(inst.graphs), len(enc.workers)
+    res = (abi.RlxSimResult * max(n, 1))()
+    lat = (C.c_double * max(n * P, 1))()
+    tok = (C.c_int64 * max(n * P, 1))()
+    util = (C.c_double * max(n * W, 1))()
+    arr = (abi.RlxSimAction * max(len(acts), 1))(*acts)
+    offs = (C.c_int64 * (n + 1))(*off)
+    rc = lib.rlx_simulate_batch(C.byref(enc.desc), C.byref(enc.graph.desc), n, offs, arr, bytes(blob) + b"\0",
+                                0 if threads is None else int(threads), res, lat, tok, util)
+    if rc != 0 and n:
+        raise RuntimeError(f"rlx status {rc}: {res[0].error.decode()}")
+    pipes = [g.pipeline_id for g in inst.graphs]
+    order = sorted(range(P), key=lambda q: pipes[q])
+    out = []
+    for s, sched in enumerate(scheds):
+        r = res[s]
+        if r.status == abi.RLX_ERR_LIMIT:
+            out.append(simulate(sched, inst))
+            continue
+        if r.status != 0:
+            msg = r.error.decode()
+            if r.status == abi.RLX_ERR_SCHEDULING:
+                raise DependencyViolationError(msg)
+            if r.status == abi.RLX_ERR_KEY:
+                raise KeyError(msg)
+            raise RuntimeError(f"rlx status {r.status}: {msg}")
+        latency = {pipes[q]: lat[s * P + q] for q in order}
+        tokens = {pipes[q]: tok[s * P + q] for q in order}
+        util_avg = {enc.workers[w]: util[s * W + w] for w in range(W)}
+        out.append(SimulationReport(makespan=r.makespan, per_pipeline_latency=latency,
+                                    per_pipeline_avg_step_latency=dict(latency),
+                                    per_pipeline_max_step_latency=dict(latency), per_pipeline_tokens=tokens,
+                                    aggregate_throughput=r.throughput, utilization_avg=util_avg,
+                                    utilization_series={}, events=[], policy=sched.policy,
+                                    metadata=dict(sched.metadata)))
+    return out
