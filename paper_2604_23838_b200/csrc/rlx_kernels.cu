@@ -238,6 +238,16 @@ RLX_HD double ediv(double d, double r, double y) {
   return fma(e, y, q0);
 }
 
+// max(0.0, z) for a non-NaN z, as Python's max(0.0, z) (-0.0 -> 0.0): the
+// sign of the bit pattern decides, with no floating-point max idiom
+RLX_HD double pos0(double z) {
+#ifdef __CUDA_ARCH__
+  return __double_as_longlong(z) > 0 ? z : 0.0;
+#else
+  return z > 0.0 ? z : 0.0;
+#endif
+}
+
 // MEM_GRID (slowdown.py:19) and DEFAULT_MEM_FRACTIONS by kind code (graph.py:98-106).
 RLX_HD double memgrid(int j) { return j == 0 ? 0.20 : j == 1 ? 0.40 : j == 2 ? 0.60 : 0.80; }
 RLX_HD double defmem(int k) {
@@ -358,6 +368,7 @@ struct Lane {
   Bits pm;    // bit 2j+s: has a non-zero prefix (value in the slice)
   Bits pf;    // bit 2j+s: still has a multiplex partner
   double tl;  // this lane's next-event candidate time
+  unsigned vmask;  // bit j: local worker j (= lane + G*j) exists
   int o, mt, ins, err;  // err: 0, RLX_ERR_SCHEDULING or key_err(...) (first failure of this candidate)
   // pass registers
   double now, last;
@@ -367,6 +378,10 @@ struct Lane {
   RLX_HD Lane(uint32_t gb, uint32_t wb, int ln, unsigned m) : gbase(gb), wbase(wb), lane(ln), gm(m) {
     err = 0;
     rb = pm = pf = 0;
+    vmask = 0;
+#pragma unroll
+    for (int j = 0; j < WPL; j++)
+      if (ln + G * j < PLAN.W) vmask |= 1u << j;
   }
 
   // ---- shared-memory views
@@ -631,16 +646,13 @@ struct Lane {
 
   // ---- selection on idle workers (one sweep)
   RLX_HD void select(bool pair) {
-    const int W = PLAN.W;
     unsigned long long* mk = mask();
     // idle local workers with a ready node: the masks load in parallel, the
     // loop below visits only workers that start something
     unsigned idle = 0;
 #pragma unroll
-    for (int j = 0; j < WPL; j++) {
-      const int w = lane + G * j;
-      if (w < W && !((rb >> (2 * j)) & Bits(3)) && mk[w] != 0ull) idle |= 1u << j;
-    }
+    for (int j = 0; j < WPL; j++)
+      if (((vmask >> j) & 1u) && !((rb >> (2 * j)) & Bits(3)) && mk[lane + G * j] != 0ull) idle |= 1u << j;
     while (idle) {
       const int j = ffs32(idle) - 1;
       idle &= idle - 1;
@@ -702,21 +714,19 @@ struct Lane {
     const bool dpos = dt > kEps;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
-      double fe[2];
+      double fe0 = INFINITY, fe1 = INFINITY;
 #pragma unroll
       for (int s = 0; s < 2; s++) {
         const Bits bit = Bits(1) << (2 * j + s);
-        fe[s] = INFINITY;
         // slot 1 (the second member of a pair) is rare: branch on it; slot 0
         // is evaluated branch-free and masked
         if (s == 1 && !(rb & bit)) continue;
         const bool on = (rb & bit) != Bits(0);
         double d = dt;
-        double p = 0.0;
         double base = now;  // now + prefix_left (:328); prefix 0 on the common path
-        bool dp = dpos;
+        bool dp = dpos, pdone = true;
         if (pm & bit) {  // pending merge prefix / realloc penalty (:330-333)
-          p = pr[2 * j + s];
+          double p = pr[2 * j + s];
           if (p > kEps) {
             const double used = d < p ? d : p;
             p = p - used;
@@ -724,7 +734,10 @@ struct Lane {
             pr[2 * j + s] = p;
             dp = d > kEps;
           }
+          // a prefix consumed to exactly 0.0 drops out: (now + 0.0) == now
+          if (p == 0.0) pm &= ~bit;
           base = now + p;
+          pdone = p <= kEps;
         }
         double wv = wk[j][s];
         const double r = rt[j][s];
@@ -732,17 +745,18 @@ struct Lane {
         // correction of d * RN(1/r) by one exact FMA residual is RN(d / r)
         // (exact for rate 1.0), so every member runs the same straight-line code
         const double q = ediv(d, r, ri[j][s]);
-        const double z = wv - q;
-        const double nw = z > 0.0 ? z : 0.0;
-        wv = (on && dp && wv > kEps) ? nw : wv;
+        // max(0.0, work_left - dt/rate) if dt > EPS and work_left > EPS; an
+        // empty slot's value is dead, so `on` is not part of the condition
+        wv = (dp && wv > kEps) ? pos0(wv - q) : wv;
         wk[j][s] = wv;
         const double prod = wv * r;  // shared by the finish test (:604-608) and the estimate (:328)
-        const bool fin = on && p <= kEps && prod <= kEps;
+        const bool fin = on && pdone && prod <= kEps;
         if (fin) fb |= bit;
-        fe[s] = (on && !fin) ? base + prod : INFINITY;
+        const double fe = (on && !fin) ? base + prod : INFINITY;
+        if (s == 0) fe0 = fe; else fe1 = fe;
       }
       const Bits both = Bits(3) << (2 * j);
-      if ((fb & both) && (rb & both) != (fb & both)) {
+      if ((pf & both) && (fb & both) && (rb & both) != (fb & both)) {
         // a survivor whose partner finished drops to its exclusive speed (:615-621)
 #pragma unroll
         for (int s = 0; s < 2; s++) {
@@ -752,12 +766,13 @@ struct Lane {
             ri[j][s] = 1.0;
             pf &= ~bit;
             const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
-            fe[s] = ((pm & bit) ? now + p : now) + wk[j][s] * 1.0;
+            const double fe = ((pm & bit) ? now + p : now) + wk[j][s] * 1.0;
+            if (s == 0) fe0 = fe; else fe1 = fe;
           }
         }
       }
-      tl = fe[0] < tl ? fe[0] : tl;
-      tl = fe[1] < tl ? fe[1] : tl;
+      tl = fe0 < tl ? fe0 : tl;
+      tl = fe1 < tl ? fe1 : tl;
     }
     rb &= ~fb;
     const int* nd = nds();
@@ -1330,7 +1345,7 @@ __global__ void __launch_bounds__(threads_for(WPL), min_blocks_for(WPL))
   const int wl = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int kNgw = 32 / G;  // groups per warp
-  const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl / G * G));
+  const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (threadIdx.x & (32 - G)));  // this group's lanes
   const uint32_t wbase = c_plan.hot_bytes + (uint32_t)warp * c_plan.w_bytes;
   const uint32_t gbase = c_plan.hot_bytes + (uint32_t)(blockDim.x >> 5) * c_plan.w_bytes + (uint32_t)grp * c_plan.g_bytes;
   if (wl == 0) {  // the warp's first candidate
