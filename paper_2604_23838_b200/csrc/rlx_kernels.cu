@@ -45,6 +45,10 @@
 #include "../../include/rlx.h"
 #include "rlx_plan.hpp"
 
+#ifndef RLX_RRS_MAXG
+#define RLX_RRS_MAXG 8
+#endif
+
 namespace rlx {
 
 // Scalars and global views of the plan; uniform reads for every lane.
@@ -340,10 +344,13 @@ RLX_HD void group_layout(DevPlan& P, int G, int WPL) {
   b += P.has_penalty ? 8u * P.W * P.P : 0u;
   P.g_pres = b;
   b += 8u * G * WPL * 2;
+  b = (b + 15u) & ~15u;  // 16-byte aligned: LDS.128 / STS.128
+  P.g_rr = b;  // (rate, RN(1/rate)) per member slot
+  b += 16u * G * WPL * 2;
   P.g_ctr = b;
   b += 4u * P.NC;
   P.g_nds = b;
-  b += 4u * G * WPL * 2;
+  b += 2u * G * WPL * 2;
   P.g_twq = b;
   b += 2u * (P.NTW + 8);
   P.g_bytes = (b + 15u) & ~15u;
@@ -363,7 +370,25 @@ struct Lane {
   const int lane;
   const unsigned gm;
   // registers: running members of this lane's workers (slot s of local worker j)
-  double wk[WPL][2], rt[WPL][2], ri[WPL][2];  // work left, rate, RN(1/rate)
+  // Where a member slot's (rate, RN(1/rate)) lives: shared memory (rr(), one
+  // LDS.128 per slot and event, relieving the register file) for groups of
+  // <= RLX_RRS_MAXG lanes, registers above (measured: config 2 / 4x4 760 vs
+  // 871 ms in shared memory; config 5 / 16x4 6.07 vs 6.49 s in registers).
+  static constexpr bool RRS = G <= RLX_RRS_MAXG;
+  double wk[WPL][2];                                  // work left
+  double rt[RRS ? 1 : WPL][2], ri[RRS ? 1 : WPL][2];  // rate, RN(1/rate) (register variant)
+  RLX_HD double2 rate_of(int j, int s) const {
+    if (RRS) return rr()[2 * j + s];
+    return make_double2(rt[RRS ? 0 : j][s], ri[RRS ? 0 : j][s]);
+  }
+  RLX_HD void set_rate_static(int j, int s, double r, double y) {  // j known at compile time
+    if (RRS) {
+      rr()[2 * j + s] = make_double2(r, y);
+    } else {
+      rt[RRS ? 0 : j][s] = r;
+      ri[RRS ? 0 : j][s] = y;
+    }
+  }
   Bits rb;    // bit 2j+s: running
   Bits pm;    // bit 2j+s: has a non-zero prefix (value in the slice)
   Bits pf;    // bit 2j+s: still has a multiplex partner
@@ -392,7 +417,8 @@ struct Lane {
   RLX_HD double* grant() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_grant); }
   RLX_HD double* pres() const { return reinterpret_cast<double*>(SMEM + gbase + PLAN.g_pres) + lane * WPL * 2; }
   RLX_HD unsigned* ctr() const { return reinterpret_cast<unsigned*>(SMEM + gbase + PLAN.g_ctr); }
-  RLX_HD int* nds() const { return reinterpret_cast<int*>(SMEM + gbase + PLAN.g_nds) + lane * WPL * 2; }
+  RLX_HD uint16_t* nds() const { return reinterpret_cast<uint16_t*>(SMEM + gbase + PLAN.g_nds) + lane * WPL * 2; }
+  RLX_HD double2* rr() const { return reinterpret_cast<double2*>(SMEM + gbase + PLAN.g_rr) + lane * WPL * 2; }
   RLX_HD uint16_t* twq() const { return reinterpret_cast<uint16_t*>(SMEM + gbase + PLAN.g_twq); }
   template <class T>
   RLX_HD const T* arr(uint32_t off) const {
@@ -419,8 +445,8 @@ struct Lane {
     return p;
   }
   RLX_HD double hdur(int n) const { return arr<double>(PLAN.o_dur)[n]; }
-  RLX_HD double hmem(int n) const { return arr<double>(PLAN.o_mem)[n]; }
-  RLX_HD double hmpre(int n) const { return arr<double>(PLAN.o_mprefix)[n]; }
+  RLX_HD double hmem(int n) const { return PLAN.mem[n]; }         // pairing only: global (L1)
+  RLX_HD double hmpre(int n) const { return PLAN.mprefix[n]; }    // member starts: global (L1)
   RLX_HD double lutv(int i) const { return arr<double>(PLAN.o_lut)[i]; }
   // node attributes (M = the candidate's virtual merged node)
   RLX_HD int kind(int n) const { return n == PLAN.M ? wc()->kind : hkind(n); }
@@ -503,11 +529,19 @@ struct Lane {
     for (int jj = 0; jj < WPL; jj++) {  // predicated register select (no per-lane branches)
       const bool hit = jj == j;
       wk[jj][s] = hit ? d : wk[jj][s];
-      rt[jj][s] = hit ? rate : rt[jj][s];
-      ri[jj][s] = hit ? rinv : ri[jj][s];
+    }
+    if (RRS) {
+      rr()[2 * j + s] = make_double2(rate, rinv);
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < (RRS ? 1 : WPL); jj++) {  // predicated register select
+        const bool hit = jj == j;
+        rt[jj][s] = hit ? rate : rt[jj][s];
+        ri[jj][s] = hit ? rinv : ri[jj][s];
+      }
     }
     const Bits bit = Bits(1) << (2 * j + s);
-    nds()[2 * j + s] = n;
+    nds()[2 * j + s] = (uint16_t)n;
     rb |= bit;
     if (partner) pf |= bit; else pf &= ~bit;
     if (pre != 0.0) {
@@ -598,8 +632,7 @@ struct Lane {
             const Bits bit = Bits(1) << (2 * j + s);
             const double r = PLAN.mrate0[2 * w + s], p = PLAN.mpre0[2 * w + s], wv = PLAN.mwork0[2 * w + s];
             nds()[2 * j + s] = PLAN.mnode0[2 * w + s];
-            rt[j][s] = r;
-            ri[j][s] = recip(r);
+            set_rate_static(j, s, r, recip(r));
             wk[j][s] = wv;
             rb |= bit;
             if (PLAN.mpart0[2 * w + s]) pf |= bit;
@@ -671,8 +704,7 @@ struct Lane {
           if (pipe(y) != px) {
             if (x != PLAN.M && y != PLAN.M) {  // decision-invariant pair: planner table
               const int cnt = arr<uint8_t>(PLAN.o_ord_cnt)[w];
-              const int ent = arr<uint8_t>(PLAN.o_ptab)[arr<uint32_t>(PLAN.o_pt_off)[w] +
-                                                        ((recw(x, 3) >> 16) & 0xFF) * cnt + ((recw(y, 3) >> 16) & 0xFF)];
+              const int ent = PLAN.ptab[PLAN.pt_off[w] + ((recw(x, 3) >> 16) & 0xFF) * cnt + ((recw(y, 3) >> 16) & 0xFF)];
               if (ent >= 0x60 && ent < 0x80) {
                 if (err < kErrKeyBase)  // the first LUT lookup of _best_pair_action that misses
                   err = (ent & 1) ? key_err(hkind(y), hkind(x)) : key_err(hkind(x), hkind(y));
@@ -714,7 +746,8 @@ struct Lane {
     const bool dpos = dt > kEps;
 #pragma unroll
     for (int j = 0; j < WPL; j++) {
-      double fe0 = INFINITY, fe1 = INFINITY;
+      double fe0 = 0.0, fe1 = 0.0;  // next finish estimates; count only where keep
+      bool keep0 = false, keep1 = false;
 #pragma unroll
       for (int s = 0; s < 2; s++) {
         const Bits bit = Bits(1) << (2 * j + s);
@@ -740,11 +773,12 @@ struct Lane {
           pdone = p <= kEps;
         }
         double wv = wk[j][s];
-        const double r = rt[j][s];
+        const double2 ry = rate_of(j, s);
+        const double r = ry.x;
         // dt / rate (:335), correctly rounded without a division: Markstein's
         // correction of d * RN(1/r) by one exact FMA residual is RN(d / r)
         // (exact for rate 1.0), so every member runs the same straight-line code
-        const double q = ediv(d, r, ri[j][s]);
+        const double q = ediv(d, r, ry.y);
         // max(0.0, work_left - dt/rate) if dt > EPS and work_left > EPS; an
         // empty slot's value is dead, so `on` is not part of the condition
         wv = (dp && wv > kEps) ? pos0(wv - q) : wv;
@@ -752,8 +786,14 @@ struct Lane {
         const double prod = wv * r;  // shared by the finish test (:604-608) and the estimate (:328)
         const bool fin = on && pdone && prod <= kEps;
         if (fin) fb |= bit;
-        const double fe = (on && !fin) ? base + prod : INFINITY;
-        if (s == 0) fe0 = fe; else fe1 = fe;
+        const double fe = base + prod;
+        if (s == 0) {
+          fe0 = fe;
+          keep0 = on && !fin;
+        } else {
+          fe1 = fe;
+          keep1 = on && !fin;
+        }
       }
       const Bits both = Bits(3) << (2 * j);
       if ((pf & both) && (fb & both) && (rb & both) != (fb & both)) {
@@ -762,8 +802,7 @@ struct Lane {
         for (int s = 0; s < 2; s++) {
           const Bits bit = Bits(1) << (2 * j + s);
           if ((rb & bit) && !(fb & bit) && (pf & bit)) {
-            rt[j][s] = 1.0;
-            ri[j][s] = 1.0;
+            set_rate_static(j, s, 1.0, 1.0);
             pf &= ~bit;
             const double p = (pm & bit) ? pr[2 * j + s] : 0.0;
             const double fe = ((pm & bit) ? now + p : now) + wk[j][s] * 1.0;
@@ -771,11 +810,11 @@ struct Lane {
           }
         }
       }
-      tl = fe0 < tl ? fe0 : tl;
-      tl = fe1 < tl ? fe1 : tl;
+      tl = (keep0 && fe0 < tl) ? fe0 : tl;
+      tl = (keep1 && fe1 < tl) ? fe1 : tl;
     }
     rb &= ~fb;
-    const int* nd = nds();
+    const uint16_t* nd = nds();
     while (fb) {
       const int i = (sizeof(Bits) == 4 ? ffs32((unsigned)fb) : ffs64(fb)) - 1;
       fb &= fb - 1;

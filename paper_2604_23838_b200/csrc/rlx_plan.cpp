@@ -550,18 +550,19 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.lut = B.put(in->lut, sizeof(double) * RLX_NKIND * RLX_NPARTNER * RLX_NALLOC);
   L.alloc_mem = B.put(in->alloc_mem, sizeof(double) * RLX_NALLOC);
   L.dur = B.putv(dur);
-  L.mem = B.putv(mem);
-  L.mprefix = B.putv(mpre);
   L.rec = B.putv(rec);
   L.ord = B.putv(ord);
   L.tw_slot = B.putv(twslot);
   L.tw_node = B.putv(twnode);
-  L.pt_off = B.putv(pt_off);
   L.ord_cnt = B.putv(ordcnt);
-  L.ptab = B.putv(ptab);
   L.succ = B.putv(sl);
   L.hot_end = (B.buf.size() + 15) & ~size_t(15);
   B.buf.resize(L.hot_end);
+  // read only by member starts and pairing: global memory (L1-resident)
+  L.mem = B.putv(mem);
+  L.mprefix = B.putv(mpre);
+  L.pt_off = B.putv(pt_off);
+  L.ptab = B.putv(ptab);
   // cold copies for the candidate prologues (global loads)
   L.succ_off = B.putv(soff);
   L.kind = B.putv(kind);
@@ -679,6 +680,8 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.frags = at<uint16_t>(base, L.frags);
   d.combos = at<uint16_t>(base, L.combos);
   d.binom = at<uint64_t>(base, L.binom);
+  d.pt_off = at<uint32_t>(base, L.pt_off);
+  d.ptab = at<uint8_t>(base, L.ptab);
   d.ctr_idx = at<uint16_t>(base, L.ctr_idx);
   d.ctr0 = at<uint16_t>(base, L.ctr0);
   d.hot = base;
@@ -688,14 +691,10 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.o_succ = (uint32_t)L.succ;
   d.o_ord = (uint32_t)L.ord;
   d.o_dur = (uint32_t)L.dur;
-  d.o_mem = (uint32_t)L.mem;
-  d.o_mprefix = (uint32_t)L.mprefix;
   d.o_lut = (uint32_t)L.lut;
   d.o_alloc_mem = (uint32_t)L.alloc_mem;
   d.o_tw_node = (uint32_t)L.tw_node;
-  d.o_pt_off = (uint32_t)L.pt_off;
   d.o_ord_cnt = (uint32_t)L.ord_cnt;
-  d.o_ptab = (uint32_t)L.ptab;
 }
 
 }  // namespace rlx

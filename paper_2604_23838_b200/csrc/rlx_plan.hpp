@@ -80,10 +80,9 @@ struct DevPlan {
   // copies and addresses it through these byte offsets.
   const uint8_t* hot;
   uint32_t hot_bytes;
-  uint32_t o_rec, o_tw_slot, o_succ, o_ord, o_dur, o_mem, o_mprefix, o_lut, o_alloc_mem, o_tw_node, o_pt_off, o_ptab,
-      o_ord_cnt;
+  uint32_t o_rec, o_tw_slot, o_succ, o_ord, o_dur, o_lut, o_alloc_mem, o_tw_node, o_ord_cnt;
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
-  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_ctr, g_nds, g_twq;
+  uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_rr, g_ctr, g_nds, g_twq;
   uint32_t w_bytes;  // warp slice (one candidate and its pass queue)
 
   // per local node (NT unless noted)
@@ -145,6 +144,8 @@ struct DevPlan {
   const uint16_t* frags;
   const uint16_t* combos;
   const uint64_t* binom;     // [(kMaxFrags+1) * kBinomK], saturating
+  const uint32_t* pt_off;    // [W+1] pair table offsets per worker
+  const uint8_t* ptab;       // decision-invariant _best_pair_action results (cnt x cnt per worker)
 };
 
 // Per-slice result of the scoring kernel.
