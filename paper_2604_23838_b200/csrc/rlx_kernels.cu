@@ -354,8 +354,8 @@ RLX_HD void group_layout(DevPlan& P, int G, int WPL) {
   P.g_pres = b;
   b += 8u * G * WPL * 2;
   b = (b + 15u) & ~15u;  // 16-byte aligned: LDS.128 / STS.128
-  P.g_rr = b;  // (rate, RN(1/rate)) per member slot
-  b += 16u * G * WPL * 2;
+  P.g_rr = b;  // (rate, RN(1/rate)) per member slot, when they live in shared memory
+  b += G <= RLX_RRS_MAXG ? 16u * G * WPL * 2 : 0u;
   P.g_ctr = b;
   b += 4u * P.NC;
   P.g_nds = b;
