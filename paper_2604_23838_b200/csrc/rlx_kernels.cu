@@ -57,6 +57,12 @@
 #ifndef RLX_TL_PRED
 #define RLX_TL_PRED 1
 #endif
+#ifndef RLX_POS0_MASK
+#define RLX_POS0_MASK 0  // 1: max(0, z) by sign mask (tuning)
+#endif
+#ifndef RLX_S0_BRANCH
+#define RLX_S0_BRANCH 0  // 1: skip idle slot-0 members by branch (tuning)
+#endif
 
 namespace rlx {
 
@@ -255,7 +261,12 @@ RLX_HD double ediv(double d, double r, double y) {
 // sign of the bit pattern decides, with no floating-point max idiom
 RLX_HD double pos0(double z) {
 #ifdef __CUDA_ARCH__
+#if RLX_POS0_MASK
+  const long long b = __double_as_longlong(z);
+  return __longlong_as_double(b & ~(b >> 63));  // negative (incl. -0.0) -> +0.0
+#else
   return __double_as_longlong(z) > 0 ? z : 0.0;
+#endif
 #else
   return z > 0.0 ? z : 0.0;
 #endif
@@ -455,7 +466,9 @@ struct Lane {
   }
   RLX_HD double hdur(int n) const { return arr<double>(PLAN.o_dur)[n]; }
   RLX_HD double hmem(int n) const { return PLAN.mem[n]; }         // pairing only: global (L1)
-  RLX_HD double hmpre(int n) const { return PLAN.mprefix[n]; }    // member starts: global (L1)
+  RLX_HD double hmpre(int n) const {  // member starts
+    return RLX_MPRE_HOT ? arr<double>(PLAN.o_mprefix)[n] : PLAN.mprefix[n];
+  }
   RLX_HD double lutv(int i) const { return arr<double>(PLAN.o_lut)[i]; }
   // node attributes (M = the candidate's virtual merged node)
   RLX_HD int kind(int n) const { return n == PLAN.M ? wc()->kind : hkind(n); }
@@ -763,7 +776,7 @@ struct Lane {
         const Bits bit = Bits(1) << (2 * j + s);
         // slot 1 (the second member of a pair) is rare: branch on it; slot 0
         // is evaluated branch-free and masked
-        if (s == 1 && !(rb & bit)) continue;
+        if ((s == 1 || RLX_S0_BRANCH) && !(rb & bit)) continue;
         const bool on = (rb & bit) != Bits(0);
         double d = dt;
         double base = now;  // now + prefix_left (:328); prefix 0 on the common path

@@ -556,11 +556,12 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.tw_node = B.putv(twnode);
   L.ord_cnt = B.putv(ordcnt);
   L.succ = B.putv(sl);
+  if (RLX_MPRE_HOT) L.mprefix = B.putv(mpre);
   L.hot_end = (B.buf.size() + 15) & ~size_t(15);
   B.buf.resize(L.hot_end);
   // read only by member starts and pairing: global memory (L1-resident)
   L.mem = B.putv(mem);
-  L.mprefix = B.putv(mpre);
+  if (!RLX_MPRE_HOT) L.mprefix = B.putv(mpre);
   L.pt_off = B.putv(pt_off);
   L.ptab = B.putv(ptab);
   // cold copies for the candidate prologues (global loads)
@@ -687,6 +688,7 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.hot = base;
   d.hot_bytes = (uint32_t)L.hot_end;
   d.o_rec = (uint32_t)L.rec;
+  d.o_mprefix = (uint32_t)L.mprefix;
   d.o_tw_slot = (uint32_t)L.tw_slot;
   d.o_succ = (uint32_t)L.succ;
   d.o_ord = (uint32_t)L.ord;

@@ -19,6 +19,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef RLX_MPRE_HOT
+#define RLX_MPRE_HOT 0  // 1: pending merge prefixes staged in shared memory (tuning)
+#endif
+
 #ifdef __CUDACC__
 #define RLX_HD __host__ __device__ __forceinline__
 #else
@@ -81,6 +85,7 @@ struct DevPlan {
   const uint8_t* hot;
   uint32_t hot_bytes;
   uint32_t o_rec, o_tw_slot, o_succ, o_ord, o_dur, o_lut, o_alloc_mem, o_tw_node, o_ord_cnt;
+  uint32_t o_mprefix;  // merge prefixes in the hot region (RLX_MPRE_HOT builds)
   // Group slice layout in shared memory (set at launch, rlx_kernels.cu group_layout)
   uint32_t g_bytes, g_mask, g_twend, g_grant, g_pres, g_rr, g_ctr, g_nds, g_twq;
   uint32_t w_bytes;  // warp slice (one candidate and its pass queue)
