@@ -424,6 +424,20 @@ int rlx_simulate_batch(const RlxInstanceDesc* inst, const RlxGraphDesc* graph, i
                        const int64_t* sched_off, const RlxSimAction* actions, const char* ids, int32_t n_threads,
                        RlxSimResult* results, double* pipe_latency, int64_t* pipe_tokens, double* util_avg);
 
+/* ---- brute-force oracle (rlmux/scheduler.py:1086-1226) ------------------ */
+
+/* enumerate_actions (:648-703) on a native state, in serial order: node
+ * indices in the state's index space, `alloc` = allocation index. */
+int rlx_enumerate(const RlxInstanceDesc* inst, const void* state, RlxAction* out, int64_t cap, int64_t* n_out);
+/* brute_force_schedule's search (:1172-1218) from the instance's initial
+ * state, seeded with the best seed makespan: depth-first over the
+ * deduplicated candidates and one advance, pruned by the bound and the
+ * state memo, in the reference's visiting order. `*n_out` = -1 when no
+ * schedule beats the seeds by more than EPS, else the winning actions in
+ * `out` (node indices of the replayed state, as rlx_drive's steps). */
+int rlx_branch_and_bound(const RlxInstanceDesc* inst, const RlxGraphDesc* graph, double best_makespan, int32_t cap,
+                         RlxStep* out, int32_t* n_out, double* best_out, int64_t* visited);
+
 int rlx_abi_version(void);
 int rlx_open(int device, void** handle);
 int rlx_load_instance(void* handle, const RlxInstanceDesc* inst);

@@ -2,7 +2,9 @@
 PuzzRL multiplexing scheduler (arxiv 2604.23838, reference package `rlmux`).
 
 Public surface (mirrors rlmux): lookahead_schedule, greedy_schedule,
-simulate, Instance and the domain types; `Evaluator` is the C-ABI handle.
+serial_schedule, brute_force_schedule, simulate (+ simulate_batch),
+Instance and the domain types; graphgen builds Sub-Stage Graphs from
+rollout tables on the GPU; `Evaluator` is the C-ABI handle.
 """
 
 from .model import (  # noqa: F401
@@ -34,7 +36,7 @@ from .model import (  # noqa: F401
     migration_cost,
 )
 from .instance_io import as_instance, load_instance, load_instances, save_instance  # noqa: F401
-from .scheduler import drive, greedy_schedule, lookahead_schedule  # noqa: F401
-from .sim import SimulationReport, simulate  # noqa: F401
+from .scheduler import brute_force_schedule, drive, greedy_schedule, lookahead_schedule, serial_schedule  # noqa: F401
+from .sim import SimulationReport, simulate, simulate_batch  # noqa: F401
 
 __version__ = "0.1.0"

@@ -173,7 +173,7 @@ EXPORTED = ("rlx_abi_version", "rlx_open", "rlx_load_instance", "rlx_decide", "r
             "rlx_state_create", "rlx_state_clone", "rlx_state_destroy", "rlx_state_error", "rlx_state_apply",
             "rlx_state_advance", "rlx_state_info", "rlx_state_snapshot", "rlx_state_node", "rlx_state_events",
             "rlx_state_completion", "rlx_graph_build", "rlx_graph_segments", "rlx_graph_stats", "rlx_graph_error",
-            "rlx_graph_free", "rlx_simulate_batch")
+            "rlx_graph_free", "rlx_simulate_batch", "rlx_enumerate", "rlx_branch_and_bound")
 
 
 def bind(lib: C.CDLL) -> C.CDLL:
@@ -239,6 +239,13 @@ def bind(lib: C.CDLL) -> C.CDLL:
                                        C.POINTER(C.c_int64), C.POINTER(RlxSimAction), C.c_char_p, C.c_int32,
                                        C.POINTER(RlxSimResult), C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double)]
+    lib.rlx_enumerate.restype = C.c_int
+    lib.rlx_enumerate.argtypes = [C.POINTER(RlxInstanceDesc), C.c_void_p, C.POINTER(RlxAction), C.c_int64,
+                                  C.POINTER(C.c_int64)]
+    lib.rlx_branch_and_bound.restype = C.c_int
+    lib.rlx_branch_and_bound.argtypes = [C.POINTER(RlxInstanceDesc), C.POINTER(RlxGraphDesc), C.c_double, C.c_int32,
+                                         C.POINTER(RlxStep), C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int64)]
     lib.rlx_state_completion.restype = C.c_int
     lib.rlx_state_completion.argtypes = [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_double)]
     return lib

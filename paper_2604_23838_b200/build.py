@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librlx.so")
-SOURCES = ("rlx_abi.cu", "rlx_kernels.cu", "rlx_plan.cpp", "rlx_state.cpp", "rlx_graph.cu", "rlx_sim.cpp")
+SOURCES = ("rlx_abi.cu", "rlx_kernels.cu", "rlx_plan.cpp", "rlx_state.cpp", "rlx_graph.cu", "rlx_sim.cpp", "rlx_bnb.cpp")
 HEADERS = ("rlx_plan.hpp", "rlx_hostplan.hpp", "rlx_state.hpp")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 

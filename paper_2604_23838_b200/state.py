@@ -251,6 +251,24 @@ class State:
             out.append((st.start, act))
         return out
 
+    def enumerate_raw(self) -> list:
+        """enumerate_actions (scheduler.py:648-703) of this state, natively:
+        RlxAction records in serial order (node indices = state indices)."""
+        n = C.c_int64()
+        self.lib.rlx_enumerate(C.byref(self.enc.desc), self.handle, None, 0, C.byref(n))
+        buf = (abi.RlxAction * max(n.value, 1))()
+        self.lib.rlx_enumerate(C.byref(self.enc.desc), self.handle, buf, n.value, C.byref(n))
+        return list(buf[: n.value])
+
+    def run_to_completion(self) -> None:
+        """ExecState.run_to_completion (scheduler.py:629-634)."""
+        while not self.done():
+            if not self.has_events():
+                done = self.completion_times()
+                stuck = sorted(set(self.alive_ids()) - set(done))
+                raise SchedulingError(f"stuck with nothing running; pending: {stuck[:4]}")
+            self.advance()
+
     def advance(self, until: float | None = None) -> None:
         rc = self.lib.rlx_state_advance(self.handle, 0 if until is None else 1, 0.0 if until is None else float(until))
         if rc != 0:
