@@ -153,7 +153,7 @@ def class_ranges(n_mux, n_merge, n_excl):
 
 
 # share of the CPU budget per class (merges cost 3(1+F) passes, the others 3)
-_CLASS_SHARE = {"merge": 0.6, "multiplex": 0.3, "exclusive": 0.1}
+_CLASS_SHARE = {"merge": 0.75, "multiplex": 0.2, "exclusive": 0.05}
 
 
 def cpu_stratified(inst, state, window, cap, counts, seconds, seed=0):
