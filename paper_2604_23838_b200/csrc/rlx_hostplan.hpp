@@ -27,8 +27,8 @@ struct Blob {
 struct PlanLayout {
   size_t kind, pipe, worker, flags, dur, mem, mprefix, suffix, msx, migc, rem, act, name_rank, lt_merge, id_off,
       ids, pos, tw_slot, tw_node, succ_off, succ, pend0, ord, ord_cnt, mask0, nmem0, mnode0, mpart0, mrate0, mpre0,
-      mwork0, worker_ids, tw_end0, grant0, pipe_rank, latency, latency_ok, has_spec, lut, alloc_mem, mux_a, mux_b,
-      mux_alloc, excl, blocks, frags, combos, binom, ctr_idx, ctr0, pt_off, ptab, rec;
+      mwork0, worker_ids, tw_end0, grant0, pipe_rank, latency, latency_ok, has_spec, lut, alloc_mem, mux_pairs,
+      excl, blocks, frags, combos, binom, ctr_idx, ctr0, pt_off, ptab, rec;
   size_t hot_end;
 };
 
@@ -39,8 +39,8 @@ struct HostPlan {
   std::vector<int> l2g;  // local -> state node index
   std::vector<int> g2l;
   // host copies for decoding
-  std::vector<uint16_t> mux_a, mux_b, excl, frags, combos;
-  std::vector<uint8_t> mux_alloc;
+  std::vector<uint16_t> excl, frags, combos;
+  std::vector<MuxPair> mux_pairs;
   std::vector<MergeBlock> blocks;
   std::vector<uint64_t> binom;
   std::vector<uint16_t> worker_of;  // [NL]

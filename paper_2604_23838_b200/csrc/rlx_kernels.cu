@@ -57,6 +57,9 @@
 #ifndef RLX_TL_PRED
 #define RLX_TL_PRED 1
 #endif
+#ifndef RLX_SEL_UNROLL
+#define RLX_SEL_UNROLL 0  // 1: selection unrolled over local workers (tuning)
+#endif
 #ifndef RLX_POS0_MASK
 #define RLX_POS0_MASK 0  // 1: max(0, z) by sign mask (tuning)
 #endif
@@ -708,53 +711,66 @@ struct Lane {
 #pragma unroll
     for (int j = 0; j < WPL; j++)
       if (((vmask >> j) & 1u) && !((rb >> (2 * j)) & Bits(3)) && mk[lane + G * j] != 0ull) idle |= 1u << j;
+#if RLX_SEL_UNROLL
+    // one copy per local worker: start() writes the member's registers with a
+    // compile-time slot instead of predicated selects over every slot
+#pragma unroll
+    for (int j = 0; j < WPL; j++)
+      if ((idle >> j) & 1u) select_one(j, pair, mk);
+#else
     while (idle) {
       const int j = ffs32(idle) - 1;
       idle &= idle - 1;
-      const int w = lane + G * j;
-      unsigned long long m = mk[w];
-      const int p = ffs64(m) - 1;
-      const int x = node_at(w, p);
-      int first = x, second = -1, al = 0;
-      bool paired = false;
-      if (pair) {
-        unsigned long long m2 = m & (m - 1);
-        const int px = pipe(x);
-        while (m2) {
-          const int q = ffs64(m2) - 1;
-          const int y = node_at(w, q);
-          if (pipe(y) != px) {
-            if (x != PLAN.M && y != PLAN.M) {  // decision-invariant pair: planner table
-              const int cnt = arr<uint8_t>(PLAN.o_ord_cnt)[w];
-              const int ent = PLAN.ptab[PLAN.pt_off[w] + ((recw(x, 3) >> 16) & 0xFF) * cnt + ((recw(y, 3) >> 16) & 0xFF)];
-              if (ent >= 0x60 && ent < 0x80) {
-                if (err < kErrKeyBase)  // the first LUT lookup of _best_pair_action that misses
-                  err = (ent & 1) ? key_err(hkind(y), hkind(x)) : key_err(hkind(x), hkind(y));
-              } else if (ent) {
-                paired = true;
-                al = ent & 31;
-                first = (ent & 0x40) ? y : x;
-                second = (ent & 0x40) ? x : y;
-              }
-            } else {
-              paired = best_pair(x, y, first, second, al);
+      select_one(j, pair, mk);
+    }
+#endif
+  }
+
+  // start the first ready node (or the best pair, pair variant) on idle local worker j
+  RLX_HD void select_one(int j, bool pair, unsigned long long* mk) {
+    const int w = lane + G * j;
+    unsigned long long m = mk[w];
+    const int p = ffs64(m) - 1;
+    const int x = node_at(w, p);
+    int first = x, second = -1, al = 0;
+    bool paired = false;
+    if (pair) {
+      unsigned long long m2 = m & (m - 1);
+      const int px = pipe(x);
+      while (m2) {
+        const int q = ffs64(m2) - 1;
+        const int y = node_at(w, q);
+        if (pipe(y) != px) {
+          if (x != PLAN.M && y != PLAN.M) {  // decision-invariant pair: planner table
+            const int cnt = arr<uint8_t>(PLAN.o_ord_cnt)[w];
+            const int ent = PLAN.ptab[PLAN.pt_off[w] + ((recw(x, 3) >> 16) & 0xFF) * cnt + ((recw(y, 3) >> 16) & 0xFF)];
+            if (ent >= 0x60 && ent < 0x80) {
+              if (err < kErrKeyBase)  // the first LUT lookup of _best_pair_action that misses
+                err = (ent & 1) ? key_err(hkind(y), hkind(x)) : key_err(hkind(x), hkind(y));
+            } else if (ent) {
+              paired = true;
+              al = ent & 31;
+              first = (ent & 0x40) ? y : x;
+              second = (ent & 0x40) ? x : y;
             }
-            if (paired) m &= ~(1ull << q);
-            break;
+          } else {
+            paired = best_pair(x, y, first, second, al);
           }
-          m2 &= m2 - 1;
+          if (paired) m &= ~(1ull << q);
+          break;
         }
+        m2 &= m2 - 1;
       }
-      m &= ~(1ull << p);
-      mk[w] = m;
-      if (paired) {
-        const double ra = L3(kind(first), kind(second), al);
-        const double rbv = L3(kind(second), kind(first), al + 12);
-        start(j, 0, w, first, ra, al, true);
-        start(j, 1, w, second, rbv, al + 12, true);
-      } else {
-        start(j, 0, w, x, L3(kind(x), -1, 0), 0, false);
-      }
+    }
+    m &= ~(1ull << p);
+    mk[w] = m;
+    if (paired) {
+      const double ra = L3(kind(first), kind(second), al);
+      const double rbv = L3(kind(second), kind(first), al + 12);
+      start(j, 0, w, first, ra, al, true);
+      start(j, 1, w, second, rbv, al + 12, true);
+    } else {
+      start(j, 0, w, x, L3(kind(x), -1, 0), 0, false);
     }
   }
 

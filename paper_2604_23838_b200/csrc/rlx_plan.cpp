@@ -375,8 +375,9 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   }
   const double h = in->headroom;
   static const double MG[4] = {0.20, 0.40, 0.60, 0.80};
-  hp.mux_a.clear(); hp.mux_b.clear(); hp.mux_alloc.clear(); hp.excl.clear();
+  hp.mux_pairs.clear(); hp.excl.clear();
   hp.frags.clear(); hp.combos.clear(); hp.blocks.clear();
+  int64_t n_mux = 0;
   for (int w = 0; w < W; w++) {
     if (nmem0[w]) continue;
     std::vector<int> g;
@@ -387,19 +388,22 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
         int a = g[x], b = g[y];
         if (pipe[a] == pipe[b]) continue;
         if (!(mem[a] + mem[b] <= 1.0 - h + 1e-12)) continue;
-        for (int o = 0; o < 2; o++) {
-          int f = o ? b : a, s = o ? a : b;
-          for (int ai = 0; ai < 3; ai++)
-            for (int mj = 0; mj < 4; mj++) {
-              if (MG[mj] + mem[s] > 1.0 - h + kEps) continue;
-              hp.mux_a.push_back((uint16_t)f);
-              hp.mux_b.push_back((uint16_t)s);
-              hp.mux_alloc.push_back((uint8_t)(1 + ai * 4 + mj));
-            }
-        }
+        int nf[2] = {0, 0};  // feasible MEM_GRID prefix for the second member
+        for (int o = 0; o < 2; o++)
+          for (int mj = 0; mj < 4; mj++)
+            if (MG[mj] + mem[o ? a : b] <= 1.0 - h + kEps) nf[o] = mj + 1;
+        if (nf[0] + nf[1] == 0) continue;
+        MuxPair mp;
+        memset(&mp, 0, sizeof mp);
+        mp.serial0 = n_mux;
+        mp.a = (uint16_t)a;
+        mp.b = (uint16_t)b;
+        mp.na = (uint8_t)nf[0];
+        mp.nb = (uint8_t)nf[1];
+        hp.mux_pairs.push_back(mp);
+        n_mux += 3 * (nf[0] + nf[1]);
       }
   }
-  const int64_t n_mux = (int64_t)hp.mux_a.size();
   fill_binom(hp.binom);
   const int64_t LIMIT = int64_t(1) << 61;
   int64_t serial = n_mux;
@@ -491,6 +495,7 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   d.realloc_penalty = in->realloc_penalty;
   d.default_migration_cost = in->default_migration_cost;
   d.n_mux = n_mux;
+  d.n_mux_pairs = (int64_t)hp.mux_pairs.size();
   d.n_merge = n_merge;
   d.n_excl = n_excl;
   d.n_total = n_mux + n_merge + n_excl;
@@ -597,9 +602,7 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   L.latency = B.put(in->latency, sizeof(double) * P * 3);
   L.latency_ok = B.put(in->latency_ok, P * 3);
   L.has_spec = B.put(in->has_spec, P);
-  L.mux_a = B.putv(hp.mux_a);
-  L.mux_b = B.putv(hp.mux_b);
-  L.mux_alloc = B.putv(hp.mux_alloc);
+  L.mux_pairs = B.putv(hp.mux_pairs);
   L.excl = B.putv(hp.excl);
   L.blocks = B.putv(hp.blocks);
   L.frags = B.putv(hp.frags);
@@ -673,9 +676,7 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.has_spec = at<uint8_t>(base, L.has_spec);
   d.lut = at<double>(base, L.lut);
   d.alloc_mem = at<double>(base, L.alloc_mem);
-  d.mux_a = at<uint16_t>(base, L.mux_a);
-  d.mux_b = at<uint16_t>(base, L.mux_b);
-  d.mux_alloc = at<uint8_t>(base, L.mux_alloc);
+  d.mux_pairs = at<MuxPair>(base, L.mux_pairs);
   d.excl = at<uint16_t>(base, L.excl);
   d.blocks = at<MergeBlock>(base, L.blocks);
   d.frags = at<uint16_t>(base, L.frags);

@@ -54,6 +54,18 @@ struct NodeRec {
   uint32_t x, y, z, w;
 };
 
+// One multiplex pair block of the candidate space (enumerate_actions
+// :661-677): nodes a < b (ready order) on one idle worker; orientation
+// (a, b) contributes 3 x na serials (alpha x the na feasible memory grid
+// points for b — a prefix of MEM_GRID), then (b, a) 3 x nb. The device
+// unranks a multiplex serial from these blocks.
+struct MuxPair {
+  int64_t serial0;
+  uint16_t a, b;
+  uint8_t na, nb;
+  uint16_t _pad;
+};
+
 struct MergeBlock {
   int64_t serial0;   // first serial of the block
   int64_t combos;    // valid combos (each has `size` targets)
@@ -141,9 +153,8 @@ struct DevPlan {
   const double* alloc_mem;   // [25]
 
   // candidate space
-  const uint16_t* mux_a;     // [n_mux]
-  const uint16_t* mux_b;
-  const uint8_t* mux_alloc;
+  const MuxPair* mux_pairs;  // [n_mux_pairs]
+  int64_t n_mux_pairs;
   const uint16_t* excl;      // [n_excl]
   const MergeBlock* blocks;  // [n_blocks]
   const uint16_t* frags;
@@ -207,10 +218,20 @@ RLX_HD uint64_t binom_at(const uint64_t* binom, int n, int k) {
 RLX_HD bool decode_serial(const DevPlan& P, int64_t s, Cand& c) {
   if (s < 0 || s >= P.n_total) return false;
   if (s < P.n_mux) {
+    int64_t lo = 0, hi = P.n_mux_pairs - 1;
+    while (lo < hi) {  // last pair block with serial0 <= s
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (P.mux_pairs[mid].serial0 <= s) lo = mid; else hi = mid - 1;
+    }
+    const MuxPair& B = P.mux_pairs[lo];
+    int r = (int)(s - B.serial0);
+    const bool o = r >= 3 * B.na;
+    if (o) r -= 3 * B.na;
+    const int n = o ? B.nb : B.na;
     c.cls = 0;
-    c.a = P.mux_a[s];
-    c.b = P.mux_b[s];
-    c.alloc = P.mux_alloc[s];
+    c.a = o ? B.b : B.a;
+    c.b = o ? B.a : B.b;
+    c.alloc = 1 + (r / n) * 4 + r % n;
     c.k = 0;
     return true;
   }
