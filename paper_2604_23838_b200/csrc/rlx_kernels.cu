@@ -60,6 +60,19 @@
 #ifndef RLX_SEL_UNROLL
 #define RLX_SEL_UNROLL 0  // 1: selection unrolled over local workers (tuning)
 #endif
+#ifndef RLX_COLD_NOINLINE
+#define RLX_COLD_NOINLINE 0
+#endif
+// Candidate-boundary routines (once per candidate) out of line (tuning knob):
+// config 2 shows 41% stall_no_instructions, but calling them measured 2-3%
+// slower than inlining (profiles/r02_ab_misc_variants.txt).
+#if RLX_COLD_NOINLINE && defined(__CUDA_ARCH__)
+#define RLX_COLD __host__ __device__ __noinline__
+#elif RLX_COLD_NOINLINE && defined(__CUDACC__)
+#define RLX_COLD __host__ __device__ inline  // host copy emitted only where used (the twin)
+#else
+#define RLX_COLD RLX_HD
+#endif
 #ifndef RLX_POS0_MASK
 #define RLX_POS0_MASK 0  // 1: max(0, z) by sign mask (tuning)
 #endif
@@ -1204,7 +1217,7 @@ RLX_HD long long work_serial(const WorkDesc& wd, long long idx) {
 // mark the warp done (gen = -1). Once some candidate failed, only lower
 // serials can still change the outcome (the reference raises on the first
 // failing serial of its scan).
-RLX_HD void fetch_candidate(const WorkDesc& wd, WarpCand* c) {
+RLX_COLD void fetch_candidate(const WorkDesc& wd, WarpCand* c) {
   const long long total = wd.loc[0] + wd.loc[1] + wd.loc[2];
   long long serial = -1;
   for (;;) {
@@ -1230,7 +1243,7 @@ RLX_HD void fetch_candidate(const WorkDesc& wd, WarpCand* c) {
 
 // Finalise the warp's candidate: key (cost, finish, priority, serial) into
 // this group's running best, or the failure into the launch's error key.
-RLX_HD void finish_candidate(const WorkDesc& wd, WarpCand* c, GroupCand* g) {
+RLX_COLD void finish_candidate(const WorkDesc& wd, WarpCand* c, GroupCand* g) {
   if (c->serial < 0) return;
   const int code = c->cerr ? c->cerr : (c->err != 0x7fffffff ? (c->err & 0xff) : 0);
   if (code) {
