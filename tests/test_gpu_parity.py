@@ -158,6 +158,21 @@ def test_livelock_matches_oracle(Evaluator, cfg, window):
             Oracle(inst).score(st, window, 3, serials=[s])
     if cfg != "config4":
         return
+    # a second livelocking candidate after the first: a shard holding both
+    # names the lower one (the reference's serial scan raises on it first)
+    n_all = ev.count(st, 3, 3)
+    try:
+        ev.decide(st, window, 3, shard=(serial + 1, n_all))
+        second = None
+    except SchedulingError as exc:
+        second = exc.serial
+    assert second is not None and second > serial, "expected a second livelocking candidate at config 4"
+    with pytest.raises(OracleError):
+        Oracle(inst).score(st, window, 3, serials=[second])
+    for b in (serial - 500, serial):
+        with pytest.raises(SchedulingError) as e3:
+            ev.decide(st, window, 3, shard=(b, second + 1))
+        assert e3.value.serial == serial
     # non-merge candidates of the same decision score normally
     n_mux = ev.count(st, 3, 3)
     ev.decide(st, 3, 3, shard=(0, 64), want_keys=True)
