@@ -73,16 +73,6 @@
 #else
 #define RLX_COLD RLX_HD
 #endif
-#ifndef RLX_BPAIR_NOINLINE
-#define RLX_BPAIR_NOINLINE 0
-#endif
-#if RLX_BPAIR_NOINLINE && defined(__CUDA_ARCH__)
-#define RLX_BPAIR __host__ __device__ __noinline__  // pairing with the merged node: rare (tuning)
-#elif RLX_BPAIR_NOINLINE && defined(__CUDACC__)
-#define RLX_BPAIR __host__ __device__ inline
-#else
-#define RLX_BPAIR RLX_HD
-#endif
 #ifndef RLX_POS0_MASK
 #define RLX_POS0_MASK 0  // 1: max(0, z) by sign mask (tuning)
 #endif
@@ -610,7 +600,7 @@ struct Lane {
   }
 
   // _best_pair_action :803-828
-  RLX_BPAIR bool best_pair(int a, int b, int& first, int& second, int& alloc) {
+  RLX_HD bool best_pair(int a, int b, int& first, int& second, int& alloc) {
     const double hr = PLAN.headroom;
     const double ma = memf(a), mb = memf(b);
     if (!(ma + mb <= 1.0 - hr + 1e-12)) return false;
