@@ -28,7 +28,7 @@ struct PlanLayout {
   size_t kind, pipe, worker, flags, dur, mem, mprefix, suffix, msx, migc, rem, act, name_rank, lt_merge, id_off,
       ids, pos, tw_slot, tw_node, succ_off, succ, pend0, ord, ord_cnt, mask0, nmem0, mnode0, mpart0, mrate0, mpre0,
       mwork0, worker_ids, tw_end0, grant0, pipe_rank, latency, latency_ok, has_spec, lut, alloc_mem, mux_pairs,
-      excl, blocks, frags, combos, binom, ctr_idx, ctr0, pt_off, ptab, rec;
+      excl, blocks, frags, combos, binom, ctr_idx, ctr0, pt_off, ptab, rec, rlut;
   size_t hot_end;
 };
 

@@ -79,6 +79,27 @@
 #ifndef RLX_S0_BRANCH
 #define RLX_S0_BRANCH 0  // 1: skip idle slot-0 members by branch (tuning)
 #endif
+// Consume variant (step()). 3 (default): groups of >= RLX_PFX_MING lanes split
+// by lane — consume<true> where a running member has a pending prefix,
+// consume_lean elsewhere — and smaller groups run consume_u (measured on one
+// box: config 5 cap 2 5.19 vs 5.48 s, config 4 cap 2 0.87 vs 0.92 s for the
+// lean split, config 2 714 vs 755 ms for consume_u). 2: consume_u always;
+// 1: the split everywhere it applies; 0: the split with consume<false>.
+#ifndef RLX_LEAN
+#define RLX_LEAN 3
+#endif
+#ifndef RLX_GMIN_REDUX
+#define RLX_GMIN_REDUX 0  // 1: group minimum of event times by two 32-bit redux.sync (tuning)
+#endif
+#ifndef RLX_RLUT
+#define RLX_RLUT 1  // member starts read RN(1/rate) from the planner's table (0: __drcp_rn per start)
+#endif
+#ifndef RLX_S1_PRED
+#define RLX_S1_PRED 1  // consume_lean evaluates slot 1 predicated (1) or by branch (0)
+#endif
+#ifndef RLX_S1_PRED_U
+#define RLX_S1_PRED_U 0  // consume_u: the same choice (measured: branch 714 vs predicated 731 ms at config 2)
+#endif
 
 namespace rlx {
 
@@ -224,11 +245,24 @@ RLX_HD unsigned gsum(unsigned m, unsigned x) {
 template <int G>
 RLX_HD double gmin(unsigned m, double t) {
 #ifdef __CUDA_ARCH__
+#if RLX_GMIN_REDUX
+  // t >= +0.0 or +inf (event times), never NaN: the u64 bit patterns order
+  // like the values, so two 32-bit warp reductions (high word, then the low
+  // word among the lanes holding the minimal high word) give the minimum
+  if (G > 1) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(t);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_min_sync(m, hi);
+    const unsigned ml = __reduce_min_sync(m, hi == mh ? lo : 0xFFFFFFFFu);
+    return __longlong_as_double((long long)((unsigned long long)mh << 32 | ml));
+  }
+#else
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) {
     double u = __shfl_xor_sync(m, t, off, G);
     t = u < t ? u : t;
   }
+#endif
 #endif
   return t;
 }
@@ -499,6 +533,18 @@ struct Lane {
     if (isnan(v) && err < kErrKeyBase) err = key_err(k, partner);
     return v;
   }
+  // (rate, RN(1/rate)) for a member start: the reciprocal comes from the
+  // planner's table (global memory, L1) instead of a division per start
+  RLX_HD double2 L3r(int k, int partner, int alloc) {
+    const int i = (k * RLX_NPARTNER + partner + 1) * RLX_NALLOC + alloc;
+    const double v = lutv(i);
+    if (isnan(v) && err < kErrKeyBase) err = key_err(k, partner);
+#if RLX_RLUT
+    return make_double2(v, PLAN.rlut[i]);
+#else
+    return make_double2(v, v == 1.0 ? 1.0 : recip(v));
+#endif
+  }
   RLX_HD int node_at(int w, int p) const {
     if (w == mt) {
       if (p == ins) return PLAN.M;
@@ -552,7 +598,8 @@ struct Lane {
 
   // ---- starting members (_start_member :460-484) on an idle local worker j
   // (dynamic); slot s is compile-time.
-  RLX_HD void start(int j, int s, int w, int n, double rate, int alloc, bool partner) {
+  RLX_HD void start(int j, int s, int w, int n, double2 rr2, int alloc, bool partner) {
+    const double rate = rr2.x, rinv = rr2.y;  // exclusive starts run at 1.0 (slowdown.py:94-99)
     double pre = mpre(n);
     if (PLAN.has_penalty && kind(n) <= RLX_KIND_DECODE_SMALL) {
       double* g = &grant()[w * PLAN.P + pipe(n)];
@@ -562,7 +609,6 @@ struct Lane {
       *g = am;
     }
     const double d = dur(n);
-    const double rinv = rate == 1.0 ? 1.0 : recip(rate);  // exclusive starts run at 1.0 (slowdown.py:94-99)
 #pragma unroll
     for (int jj = 0; jj < WPL; jj++) {  // predicated register select (no per-lane branches)
       const bool hit = jj == j;
@@ -701,12 +747,12 @@ struct Lane {
         const int j = w / G;
         if (act.cls == 2) {
           mk[w] &= ~(1ull << (act.a == PLAN.M ? ins : pos_of(act.a)));
-          start(j, 0, w, act.a, L3(kind(act.a), -1, 0), 0, false);
+          start(j, 0, w, act.a, L3r(kind(act.a), -1, 0), 0, false);
         } else {
           const int a = act.a, b = act.b;
           mk[w] &= ~((1ull << (a == PLAN.M ? ins : pos_of(a))) | (1ull << (b == PLAN.M ? ins : pos_of(b))));
-          const double ra = L3(kind(a), kind(b), act.alloc);
-          const double rbv = L3(kind(b), kind(a), act.alloc + 12);
+          const double2 ra = L3r(kind(a), kind(b), act.alloc);
+          const double2 rbv = L3r(kind(b), kind(a), act.alloc + 12);
           start(j, 0, w, a, ra, act.alloc, true);
           start(j, 1, w, b, rbv, act.alloc + 12, true);
         }
@@ -778,12 +824,12 @@ struct Lane {
     m &= ~(1ull << p);
     mk[w] = m;
     if (paired) {
-      const double ra = L3(kind(first), kind(second), al);
-      const double rbv = L3(kind(second), kind(first), al + 12);
+      const double2 ra = L3r(kind(first), kind(second), al);
+      const double2 rbv = L3r(kind(second), kind(first), al + 12);
       start(j, 0, w, first, ra, al, true);
       start(j, 1, w, second, rbv, al + 12, true);
     } else {
-      start(j, 0, w, x, L3(kind(x), -1, 0), 0, false);
+      start(j, 0, w, x, L3r(kind(x), -1, 0), 0, false);
     }
   }
 
@@ -879,6 +925,188 @@ struct Lane {
     }
   }
 
+  // ---- advance for a lane none of whose running members has a pending
+  // prefix (base == now for all of them): the arithmetic of consume<false>,
+  // laid out as straight-line phases over all member slots so that the
+  // slots' independent FP64 chains interleave instead of running worker by
+  // worker between branches:
+  //  1. consume dt (:335) and test for finish (:604-608), all slot 0s, then
+  //     the running slot 1s;
+  //  2. survivors of finished pairs drop to their exclusive speed (:615-621),
+  //     found by bit arithmetic (partner finished = the pair-swapped `fb`);
+  //  3. next finish estimate (:328): RN(now + x) is monotone in x, so
+  //     min_i RN(now + p_i) == RN(now + min_i p_i) — one add per lane, the
+  //     minimum taken over the products in two independent chains.
+  RLX_HD void consume_lean(double dt, unsigned& ld) {
+    double pd[WPL][2];
+    Bits fb = 0;  // finish test on every evaluated slot; masked by rb below
+    if (dt > kEps) {  // group-uniform: max(0, work_left - dt/rate) where work_left > EPS
+#pragma unroll
+      for (int s = 0; s < 2; s++)
+#pragma unroll
+        for (int j = 0; j < WPL; j++) {
+          if (!RLX_S1_PRED && s == 1 && !(rb & (Bits(1) << (2 * j + 1)))) continue;
+          const double2 ry = rate_of(j, s);
+          const double wv = wk[j][s];
+          const double nz = pos0(wv - ediv(dt, ry.x, ry.y));
+          wk[j][s] = wv > kEps ? nz : wv;
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; s++)
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const Bits bit = Bits(1) << (2 * j + s);
+        if (!RLX_S1_PRED && s == 1 && !(rb & bit)) {
+          pd[j][s] = INFINITY;
+          continue;
+        }
+        const double prod = wk[j][s] * rate_of(j, s).x;
+        pd[j][s] = prod;
+        fb |= prod <= kEps ? bit : Bits(0);
+      }
+    fb &= rb;
+    const Bits lo = Bits(~Bits(0) / 3u);  // slot-0 bits
+    const Bits surv = pf & rb & ~fb & (((fb & lo) << 1) | ((fb >> 1) & lo));
+    if (surv) {
+#pragma unroll
+      for (int j = 0; j < WPL; j++)
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if (surv & bit) {
+            set_rate_static(j, s, 1.0, 1.0);
+            pd[j][s] = wk[j][s];  // work_left * 1.0
+          }
+        }
+      pf &= ~surv;
+    }
+    const Bits keep = rb & ~fb;
+    double m0 = INFINITY, m1 = INFINITY;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      m0 = (((keep >> (2 * j)) & Bits(1)) && pd[j][0] < m0) ? pd[j][0] : m0;
+      m1 = (((keep >> (2 * j + 1)) & Bits(1)) && pd[j][1] < m1) ? pd[j][1] : m1;
+    }
+    tl = now + (m1 < m0 ? m1 : m0);
+    rb &= ~fb;
+    const uint16_t* nd = nds();
+    while (fb) {
+      const int i = (sizeof(Bits) == 4 ? ffs32((unsigned)fb) : ffs64(fb)) - 1;
+      fb &= fb - 1;
+      complete(nd[i], ld);
+    }
+  }
+
+  // ---- consume_lean for every lane: the running members with a pending
+  // prefix (`pmr`, rare: a merge's migration prefix, realloc penalties) are
+  // left out of the straight-line phases and finished on a slow path with
+  // consume<true>'s arithmetic, so a warp whose lanes differ no longer runs
+  // two whole consume variants.
+  RLX_HD void consume_u(double dt, unsigned& ld) {
+    double pd[WPL][2];
+    const Bits pmr = pm & rb;
+    if (dt > kEps) {
+#pragma unroll
+      for (int s = 0; s < 2; s++)
+#pragma unroll
+        for (int j = 0; j < WPL; j++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if (!RLX_S1_PRED_U && s == 1 && !(rb & bit)) continue;
+          const double2 ry = rate_of(j, s);
+          const double wv = wk[j][s];
+          const double nz = pos0(wv - ediv(dt, ry.x, ry.y));
+          wk[j][s] = (wv > kEps && !(pmr & bit)) ? nz : wv;
+        }
+    }
+    Bits fb = 0;
+#pragma unroll
+    for (int s = 0; s < 2; s++)
+#pragma unroll
+      for (int j = 0; j < WPL; j++) {
+        const Bits bit = Bits(1) << (2 * j + s);
+        if (!RLX_S1_PRED_U && s == 1 && !(rb & bit)) {
+          pd[j][s] = INFINITY;
+          continue;
+        }
+        const double prod = wk[j][s] * rate_of(j, s).x;
+        pd[j][s] = prod;
+        fb |= prod <= kEps ? bit : Bits(0);
+      }
+    fb &= rb & ~pmr;
+    double* pr = pres();
+    if (pmr) {  // prefix_left first, then work (:328-336)
+#pragma unroll
+      for (int j = 0; j < WPL; j++)
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if (!(pmr & bit)) continue;
+          double d = dt, p = pr[2 * j + s];
+          bool dp = dt > kEps;
+          if (p > kEps) {
+            const double used = d < p ? d : p;
+            p = p - used;
+            d = d - used;
+            pr[2 * j + s] = p;
+            dp = d > kEps;
+          }
+          if (p == 0.0) pm &= ~bit;  // (now + 0.0) == now: the prefix drops out
+          const double2 ry = rate_of(j, s);
+          double wv = wk[j][s];
+          const double q = ediv(d, ry.x, ry.y);
+          wv = (dp && wv > kEps) ? pos0(wv - q) : wv;
+          wk[j][s] = wv;
+          const double prod = wv * ry.x;
+          pd[j][s] = prod;
+          if (p <= kEps && prod <= kEps) fb |= bit;
+        }
+    }
+    const Bits lo = Bits(~Bits(0) / 3u);  // slot-0 bits
+    const Bits surv = pf & rb & ~fb & (((fb & lo) << 1) | ((fb >> 1) & lo));
+    if (surv) {  // a survivor whose partner finished drops to its exclusive speed (:615-621)
+#pragma unroll
+      for (int j = 0; j < WPL; j++)
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if (surv & bit) {
+            set_rate_static(j, s, 1.0, 1.0);
+            pd[j][s] = wk[j][s];  // work_left * 1.0
+          }
+        }
+      pf &= ~surv;
+    }
+    const Bits keep = rb & ~fb;
+    const Bits kf = keep & ~pmr;
+    double m0 = INFINITY, m1 = INFINITY;
+#pragma unroll
+    for (int j = 0; j < WPL; j++) {
+      m0 = (((kf >> (2 * j)) & Bits(1)) && pd[j][0] < m0) ? pd[j][0] : m0;
+      m1 = (((kf >> (2 * j + 1)) & Bits(1)) && pd[j][1] < m1) ? pd[j][1] : m1;
+    }
+    tl = now + (m1 < m0 ? m1 : m0);  // monotone: min_i RN(now + p_i) == RN(now + min_i p_i)
+    if (keep & pmr) {  // base = now + prefix_left for these
+#pragma unroll
+      for (int j = 0; j < WPL; j++)
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+          const Bits bit = Bits(1) << (2 * j + s);
+          if (keep & pmr & bit) {
+            const double fe = (now + pr[2 * j + s]) + pd[j][s];
+            tl = fe < tl ? fe : tl;
+          }
+        }
+    }
+    rb &= ~fb;
+    const uint16_t* nd = nds();
+    while (fb) {
+      const int i = (sizeof(Bits) == 4 ? ffs32((unsigned)fb) : ffs64(fb)) - 1;
+      fb &= fb - 1;
+      complete(nd[i], ld);
+    }
+  }
+
   // ---- one simulated event of _complete_window (:833-867). Returns true
   // while the pass continues; on false `now`/`last`/`any_done` hold the result.
   RLX_HD bool step(bool pair, int nwin, long long serial, int variant) {
@@ -906,8 +1134,13 @@ struct Lane {
     // box: config 5 5.70 vs 6.35 s, config 4 0.95 vs 1.08 s); with 4- and
     // 8-lane groups a warp holds 4-8 groups, some lane nearly always has a
     // prefix and the split would run both versions (config 2 875 vs 764 ms)
-    if (!(RLX_PFX_SPLIT && G >= RLX_PFX_MING) || (pm & rb))
+    constexpr bool kSplit = RLX_PFX_SPLIT && G >= RLX_PFX_MING;
+    if (RLX_LEAN == 2 || (RLX_LEAN == 3 && !kSplit))
+      consume_u(dt, ld);
+    else if (!kSplit || (pm & rb))
       consume<true>(dt, ld);
+    else if (RLX_LEAN)
+      consume_lean(dt, ld);
     else
       consume<false>(dt, ld);
     if (!has_tw) {

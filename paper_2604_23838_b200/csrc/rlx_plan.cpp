@@ -569,6 +569,11 @@ int build_plan(const RlxInstanceDesc* in, const RlxStateDesc* sd, int rounds, in
   if (!RLX_MPRE_HOT) L.mprefix = B.putv(mpre);
   L.pt_off = B.putv(pt_off);
   L.ptab = B.putv(ptab);
+  {  // RN(1 / rate) per LUT entry: a member start loads it instead of dividing
+    std::vector<double> rl(RLX_NKIND * RLX_NPARTNER * RLX_NALLOC);
+    for (size_t i = 0; i < rl.size(); i++) rl[i] = 1.0 / in->lut[i];
+    L.rlut = B.putv(rl);
+  }
   // cold copies for the candidate prologues (global loads)
   L.succ_off = B.putv(soff);
   L.kind = B.putv(kind);
@@ -684,6 +689,7 @@ void relocate(HostPlan& hp, const uint8_t* base, DevPlan& d) {
   d.binom = at<uint64_t>(base, L.binom);
   d.pt_off = at<uint32_t>(base, L.pt_off);
   d.ptab = at<uint8_t>(base, L.ptab);
+  d.rlut = at<double>(base, L.rlut);
   d.ctr_idx = at<uint16_t>(base, L.ctr_idx);
   d.ctr0 = at<uint16_t>(base, L.ctr0);
   d.hot = base;

@@ -150,6 +150,7 @@ struct DevPlan {
 
   // cost model
   const double* lut;         // [7*8*25]
+  const double* rlut;        // [7*8*25] RN(1 / lut): member starts (global, L1)
   const double* alloc_mem;   // [25]
 
   // candidate space

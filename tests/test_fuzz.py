@@ -61,12 +61,13 @@ def _key(rows):
     return cost, fin, int(k[2]) >> 61, int(k[2]) & ((1 << 61) - 1)
 
 
-def test_twin_matches_oracle_on_random_knobs():
+@pytest.mark.parametrize("variant", ["lean", "u"])
+def test_twin_matches_oracle_on_random_knobs(variant):
     from twin import Twin
 
     failures = []
     for inst, window, cap in cases(40, seed=7):
-        t = Twin(inst)
+        t = Twin(inst, variant=variant)
 
         def twin_score(state):
             rc, err, n, key, dbg, keys = t.decide(state, window, cap, shard=(0, -1))

@@ -17,8 +17,10 @@ from paper_2604_23838_b200.state import State as HostState  # noqa: E402
 from paper_2604_23838_b200.instance_io import action_to_json  # noqa: E402
 
 
-@pytest.fixture(scope="module")
-def Twin():
+@pytest.fixture(scope="module", params=["lean", "u"])
+def Twin(request):
+    """The twin class bound to one consume variant (twin/Makefile)."""
+    import functools
     import shutil
 
     if shutil.which(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")) is None and not os.path.exists(
@@ -26,14 +28,13 @@ def Twin():
         pytest.skip("nvcc not available")
     from twin import Twin as T
 
-    return T
+    return functools.partial(T, variant=request.param)
 
 
-def _twin_chooser(inst, window, cap, log):
+def _twin_chooser(Twin, inst, window, cap, log):
     import numpy as np
 
     from oracle.oracle import Oracle
-    from twin import Twin
 
     t = Twin(inst)
     o = Oracle(inst, nthreads=1)
@@ -62,7 +63,7 @@ def test_twin_golden_schedules(Twin, golden_schedules):
         if len(inst.workers()) > 32:
             continue
         log = []
-        s = drive(inst, _twin_chooser(inst, g["window"], g["max_merge"], log), "lookahead", {})
+        s = drive(inst, _twin_chooser(Twin, inst, g["window"], g["max_merge"], log), "lookahead", {})
         acts = [[t.start, action_to_json(t.action)] for t in s.actions]
         keys_ok = len(log) == len(g["decisions"]) and all(
             d["n"] == gd["n"] and list(d["key"]) == list(gd["key"]) for d, gd in zip(log, g["decisions"]))
@@ -77,7 +78,7 @@ def test_twin_golden_schedules_knobs(Twin, golden_schedules_knobs):
         g = golden_schedules_knobs[name]
         inst = instance(g["instance"])
         log = []
-        s = drive(inst, _twin_chooser(inst, g["window"], g["max_merge"], log), "lookahead", {})
+        s = drive(inst, _twin_chooser(Twin, inst, g["window"], g["max_merge"], log), "lookahead", {})
         acts = [[t.start, action_to_json(t.action)] for t in s.actions]
         if acts != g["actions"] or [d["key"] for d in log] != [list(d["key"]) for d in g["decisions"]]:
             bad.append(name)
