@@ -85,6 +85,7 @@
 // box: config 5 cap 2 5.19 vs 5.48 s, config 4 cap 2 0.87 vs 0.92 s for the
 // lean split, config 2 714 vs 755 ms for consume_u). 2: consume_u always;
 // 1: the split everywhere it applies; 0: the split with consume<false>.
+// (consume_u on the prefix lanes of the split measured no better: 5.13 s.)
 #ifndef RLX_LEAN
 #define RLX_LEAN 3
 #endif
