@@ -1,3 +1,4 @@
+# NOTE: compute-sanitizer is closed on the GPU pool (round 2): runs under it left GPUs needing a reset. Kept for the record.
 # compute-sanitizer memcheck / racecheck / synccheck on small decisions (outputs under gpurun_out/)
 set -x
 export PYTHONDONTWRITEBYTECODE=1
