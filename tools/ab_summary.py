@@ -8,7 +8,7 @@ d = collections.defaultdict(list)
 best = collections.defaultdict(set)
 order = []
 for line in open(sys.argv[1]):
-    m = re.match(r'\[(\w+) r(\d+)\] (config\d+) .*best=(\(.*?\)) .*kernel=([\d.]+)ms', line)
+    m = re.match(r'\[(\S+) r(\d+)\] (config\d+) .*best=(\(.*?\)) .*kernel=([\d.]+)ms', line)
     if m:
         v, _, c, b, k = m.groups()
         d[(c, v)].append(float(k))
