@@ -89,6 +89,9 @@
 #ifndef RLX_LEAN
 #define RLX_LEAN 3
 #endif
+#ifndef RLX_WIN_SMEM
+#define RLX_WIN_SMEM 1  // window-completion count and time in the group slice, not registers (plans without tool waits)
+#endif
 #ifndef RLX_GMIN_REDUX
 #define RLX_GMIN_REDUX 0  // 1: group minimum of event times by two 32-bit redux.sync (tuning)
 #endif
@@ -399,6 +402,7 @@ struct GroupCand {
   unsigned long long passes, ncand, events;
   int twq_n, tw_run;
   int dsum;  // window completions of the running pass (plans without tool waits)
+  double dlast;  // time of the last event with a window completion (RLX_WIN_SMEM)
 };
 
 // Warp and group slice layout (offsets in bytes), stored in the DevPlan
@@ -1108,6 +1112,16 @@ struct Lane {
     }
   }
 
+  // ---- the pass result (window_cost :889-890): the time of the last window
+  // completion, or `now` if none
+  RLX_HD double result() const {
+    if (RLX_WIN_SMEM && PLAN.NTW == 0) {
+      const GroupCand* g = gc();
+      return g->dsum > 0 ? g->dlast : now;
+    }
+    return any_done ? last : now;
+  }
+
   // ---- one simulated event of _complete_window (:833-867). Returns true
   // while the pass continues; on false `now`/`last`/`any_done` hold the result.
   RLX_HD bool step(bool pair, int nwin, long long serial, int variant) {
@@ -1148,6 +1162,17 @@ struct Lane {
       // window completions of this event: the completing lanes add to a
       // group counter before the barrier every lane needs anyway; a
       // broadcast read replaces a warp reduction on the critical path
+#if RLX_WIN_SMEM
+      // ... and record the event time next to it (every completing lane
+      // writes the same `now`), so the pass keeps no per-lane count, last
+      // time or flag in registers (they spilled to local memory)
+      if (ld) {
+        at_add<G>(&g->dsum, (int)ld);
+        g->dlast = now;
+      }
+      gsync<G>(gm);
+      return g->dsum < nwin;
+#endif
       if (G > 1 && ld) at_add<G>(&g->dsum, (int)ld);
       gsync<G>(gm);
       const int cum = G > 1 ? g->dsum : done_cnt + (int)ld;
@@ -1542,7 +1567,7 @@ struct GroupRunner {
     WarpCand* c = S.wc();
     gsync<G>(S.gm);
     if (ran) {  // fold the finished pass into the candidate
-      const double x = S.any_done ? S.last : S.now;
+      const double x = S.result();
       const int e = gmax<G>(S.gm, S.err);
       gsync<G>(S.gm);
       if (S.lane == 0) {
