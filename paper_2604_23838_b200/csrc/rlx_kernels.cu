@@ -24,9 +24,11 @@
 //    selection on idle workers (find-first-set over a 64-bit ready mask whose
 //    bit order is the completion key), group min of finish estimates
 //    (butterfly shuffles over G lanes), consume, completions (shared-memory
-//    atomics when G > 1), tool-wait expiry/auto-start, window count. The
-//    finish estimate of every member is produced in the same sweep that
-//    consumes it, so each event touches each member once.
+//    atomics when G > 1), tool-wait expiry/auto-start, window count. Consume
+//    runs as straight-line phases over a lane's member slots (consume dt and
+//    test for finish, re-rate survivors, minimum of the next finish
+//    estimates) so the slots' FP64 chains interleave (consume_lean /
+//    consume_u).
 //  * Groups pull whole candidates from a global counter, heaviest class
 //    (merges: 3*(1+F) passes) first, and keep a running minimum key.
 //
