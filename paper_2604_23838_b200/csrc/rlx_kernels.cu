@@ -1563,7 +1563,13 @@ struct GroupRunner {
       active = S.step(pair, nwin, 0, variant);
       return true;
     }
-    // ---- pass boundary. Warp-slice fields are written by one lane and read
+    return boundary() != 2;
+  }
+
+  // ---- pass boundary: fold the finished pass, claim the next one of the
+  // warp's candidate and initialise it. 0: claimed, 1: wait, 2: no more work.
+  RLX_HD int boundary() {
+    // Warp-slice fields are written by one lane and read
     // by the others after a __syncwarp / fence (compute-sanitizer racecheck).
     GroupCand* g = S.gc();
     WarpCand* c = S.wc();
@@ -1617,8 +1623,8 @@ struct GroupRunner {
       }
     }
     st = (int)gbcast<G>(S.gm, st);
-    if (st == 2) return false;
-    if (st == 1) return true;
+    if (st == 2) return 2;
+    if (st == 1) return 1;
     q = (int)gbcast<G>(S.gm, q);
     fence_block();
     int ai;
@@ -1635,7 +1641,7 @@ struct GroupRunner {
     }
     ran = true;
     active = nwin > 0;  // empty window: the pass result is `now` (:889-890)
-    return true;
+    return 0;
   }
 
   RLX_HD void finish(SliceOut* out) {
